@@ -1,0 +1,134 @@
+// Density-response accumulation (reference response.py:150-154):
+//   drho(r) = sum_b [ c2_b Re(conj psi_b(r) dphi~_b(r)) + c1_b |psi_b(r)|^2 ]
+// with dphi~_b the unnormalised inverse transform of the orbital response
+// (c2_b = w_k 2 f_n / sqrt(Omega) carries the to_real scale) and psi_b(r)
+// from the per-state cache.  The inverse x-FFT of dphi is fused into the
+// accumulation, so dphi(r) never reaches HBM; bands are reduced in a fixed
+// order inside each CTA and chunk partials are summed in a fixed order, so
+// drho is bitwise reproducible (no floating-point atomics).
+#include "state.cuh"
+
+namespace pwb {
+
+constexpr int NTA = 256;
+constexpr int kMaxOwn = 16;   // tile elements per thread (tile*nx <= 3072 + pad)
+
+__global__ void __launch_bounds__(NTA) k_drho_partial(GridDev g, int nband, int per_chunk,
+                                                      const double2* __restrict__ W,
+                                                      const double2* __restrict__ psir,
+                                                      const double* __restrict__ c2,
+                                                      const double* __restrict__ c1,
+                                                      double* __restrict__ partial) {
+  extern __shared__ double2 sm[];
+  const int T = g.tile, Tp = g.tilep, nx = g.nx, nyz = g.nyz;
+  const int t0 = blockIdx.x * T;
+  const int nt = min(T, nyz - t0);
+  const int b0 = blockIdx.y * per_chunk;
+  const int b1 = min(nband, b0 + per_chunk);
+  const int nel = nt * nx;
+  double acc[kMaxOwn];
+#pragma unroll
+  for (int q = 0; q < kMaxOwn; ++q) acc[q] = 0.0;
+  for (int b = b0; b < b1; ++b) {
+    for (int i = threadIdx.x; i < nx * Tp; i += NTA) sm[i] = make_double2(0.0, 0.0);
+    __syncthreads();
+    const double2* src = W + (size_t)b * g.nxa * nyz;
+    for (int i = threadIdx.x; i < g.nxa * nt; i += NTA) {
+      const int p = i / nt, t = i - p * nt;
+      sm[g.xa[p] * Tp + t] = src[(size_t)p * nyz + t0 + t];
+    }
+    __syncthreads();
+    fft_lines<NTA>(sm, g.px, nt, Tp, 1, nullptr, true);
+    const double a2 = c2[b], a1 = c1[b];
+    const double2* ps = psir + (size_t)b * g.ng + (size_t)t0 * nx;
+#pragma unroll
+    for (int q = 0; q < kMaxOwn; ++q) {
+      const int i = threadIdx.x + q * NTA;
+      if (i < nel) {
+        const int t = i / nx, x = i - t * nx;
+        const double2 d = sm[x * Tp + t];
+        const double2 p = ps[i];
+        acc[q] += a2 * (p.x * d.x + p.y * d.y) + a1 * (p.x * p.x + p.y * p.y);
+      }
+    }
+    __syncthreads();
+  }
+  double* out = partial + (size_t)blockIdx.y * g.ng + (size_t)t0 * nx;
+#pragma unroll
+  for (int q = 0; q < kMaxOwn; ++q) {
+    const int i = threadIdx.x + q * NTA;
+    if (i < nel) out[i] = acc[q];
+  }
+}
+
+__global__ void k_drho_reduce(int n, int nchunk, const double* __restrict__ partial,
+                              double* __restrict__ drho) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = partial[i];
+  for (int c = 1; c < nchunk; ++c) s += partial[(size_t)c * n + i];
+  drho[i] = s;
+}
+
+// out[i] = sum_b |psi_b(i)|^2  (or (Re psi_b)^2); max taken by k_max_reduce
+__global__ void k_row_sq(int n, int nband, const double2* __restrict__ psir, int real_part,
+                         double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int b = 0; b < nband; ++b) {
+    const double2 p = psir[(size_t)b * n + i];
+    s += real_part ? p.x * p.x : p.x * p.x + p.y * p.y;
+  }
+  out[i] = s;
+}
+
+__global__ void k_max_reduce(int n, const double* __restrict__ in, double* __restrict__ out) {
+  __shared__ double red[256];
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) m = fmax(m, in[i]);
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+int launch_drho_partial(pwb_grid* g, int nband, const double2* W, const double2* psir,
+                        const double* c2, const double* c1, int nchunk, double* partial) {
+  if (g->dev.tile * g->nx > kMaxOwn * NTA)
+    return fail(PWB_ERR_UNSUPPORTED, "pencil tile too large for accumulation kernel");
+  const int ntile = (g->nyz + g->dev.tile - 1) / g->dev.tile;
+  const int per = (nband + nchunk - 1) / nchunk;
+  dim3 grid(ntile, nchunk);
+  k_drho_partial<<<grid, NTA, pencil_smem(g), g->stream>>>(g->dev, nband, per, W, psir, c2, c1,
+                                                           partial);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int launch_drho_reduce(pwb_grid* g, int nchunk, const double* partial, double* drho) {
+  k_drho_reduce<<<(g->ng + 255) / 256, 256, 0, g->stream>>>(g->ng, nchunk, partial, drho);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int launch_row_norm(pwb_grid* g, int nband, const double2* psir, int real_part, double* out) {
+  PWB_TRY(g->tmp_real.ensure((size_t)(g->ng + 1) * sizeof(double)));
+  double* sq = as<double>(g->tmp_real);
+  k_row_sq<<<(g->ng + 255) / 256, 256, 0, g->stream>>>(g->ng, nband, psir, real_part, sq);
+  PWB_LAUNCH_CHECK();
+  k_max_reduce<<<1, 256, 0, g->stream>>>(g->ng, sq, out);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int configure_chi0_kernels(const pwb_grid* g) {
+  PWB_CUDA(cudaFuncSetAttribute(k_drho_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pencil_smem(g)));
+  return PWB_OK;
+}
+
+}  // namespace pwb

@@ -1,0 +1,393 @@
+// Batched, pruned 3-D FFT kernels for sphere <-> cube transforms (sm_100a).
+//
+// A sphere -> real-space transform of one band is split into
+//   plane pass  (one CTA per active x plane): scatter the sphere points of
+//               that plane into a shared-memory y-z plane, z-FFTs on the
+//               active y lines only, y-FFTs on every z line, write the plane;
+//   pencil pass (one CTA per tile of y-z points): x-FFT of length nx whose
+//               input is zero outside the active planes.
+// The H apply fuses inverse-x, *V(r)/n_g and forward-x in ONE pencil pass,
+// and the forward plane pass fuses the sphere gather with the kinetic and
+// eigenvalue-shift epilogue, so H psi costs three passes over the pruned
+// plane buffer ("Kernels").  Only nxa of nx planes (the sphere
+// occupies |ix| <= ~N/4 of the 2x-oversampled cube) are ever stored.
+#include "grid.cuh"
+
+namespace pwb {
+
+constexpr int NT = 256;
+
+// ----------------------------------------------------------------------------
+// plane pass, inverse: sphere rows -> W[b][p]
+__global__ void __launch_bounds__(NT) k_plane_inv(GridDev g, const double2* __restrict__ psi,
+                                                  const double2* __restrict__ psi2,
+                                                  const int* __restrict__ band_k, double scale,
+                                                  double2* __restrict__ W) {
+  extern __shared__ double2 sm[];
+  const int p = blockIdx.x;
+  const int b = blockIdx.y;
+  const int k = band_k ? band_k[b] : 0;
+  const int nyz = g.nyz;
+  for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const int s0 = g.xr[k * (g.nxa + 1) + p];
+  const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
+  const double2* src = psi + (size_t)b * g.nbp;
+  const int* pp = g.pp + (size_t)k * g.nbp;
+  if (psi2) {
+    const double2* src2 = psi2 + (size_t)b * g.nbp;
+    for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(cadd(src[s], src2[s]), scale);
+  } else {
+    for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(src[s], scale);
+  }
+  __syncthreads();
+  fft_lines<NT>(sm, g.pz, g.nya, g.ny, 0, g.ya, true);   // z lines of active y
+  fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, true);  // y lines, every z
+  double2* dst = W + ((size_t)b * g.nxa + p) * nyz;
+  for (int i = threadIdx.x; i < nyz; i += NT) dst[i] = sm[i];
+}
+
+// plane pass, forward: W[b][p] -> sphere rows with epilogue
+//   out[s] = a * F(W)[pp[s]] + (kin[s] - shift[b]) * psi_in[s]
+__global__ void __launch_bounds__(NT) k_plane_fwd(GridDev g, const double2* __restrict__ W,
+                                                  const int* __restrict__ band_k, double a,
+                                                  const double2* __restrict__ psi_in,
+                                                  const double* __restrict__ shift,
+                                                  double2* __restrict__ out) {
+  extern __shared__ double2 sm[];
+  const int p = blockIdx.x;
+  const int b = blockIdx.y;
+  const int k = band_k ? band_k[b] : 0;
+  const int nyz = g.nyz;
+  const double2* srcw = W + ((size_t)b * g.nxa + p) * nyz;
+  for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = srcw[i];
+  __syncthreads();
+  fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, false);  // y lines, every z
+  fft_lines<NT>(sm, g.pz, g.nya, g.ny, 0, g.ya, false);    // z lines of active y
+  const int s0 = g.xr[k * (g.nxa + 1) + p];
+  const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
+  const int* pp = g.pp + (size_t)k * g.nbp;
+  const double* kin = g.kin + (size_t)k * g.nbp;
+  double2* dst = out + (size_t)b * g.nbp;
+  const double sh = shift ? shift[b] : 0.0;
+  if (psi_in) {
+    const double2* pin = psi_in + (size_t)b * g.nbp;
+    for (int s = s0 + threadIdx.x; s < s1; s += NT) {
+      const double2 v = sm[pp[s]];
+      const double2 q = pin[s];
+      const double d = kin[s] - sh;
+      dst[s] = make_double2(a * v.x + d * q.x, a * v.y + d * q.y);
+    }
+  } else {
+    for (int s = s0 + threadIdx.x; s < s1; s += NT) dst[s] = cscale(sm[pp[s]], a);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// pencil pass.  IN: 0 = W rows (plane list xin), 1 = natural complex,
+// 2 = natural real.  OUT: 0 = W rows (plane list xout), 1 = natural complex,
+// 2 = natural real part (+ LDA term).  mode: 0 none, 1 fwd, 2 inv,
+// 3 inv -> *v*vscale -> fwd.
+struct PencilArgs {
+  const double2* win;
+  const double2* cin;
+  const double* rin;
+  const int* xin;
+  int nxin;
+  size_t in_stride;  // elements per band
+  const double* v;
+  double vscale;
+  int mode;
+  double2* wout;
+  double2* cout;
+  double* rout;
+  const int* xout;
+  int nxout;
+  size_t out_stride;
+  double oscale;
+  const double* lda_v;    // optional: rout += lda_c * max(rho,1e-10)^(-2/3) * lda_v
+  const double* lda_rho;
+  double lda_c;
+};
+
+template <int IN, int OUT>
+__global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
+  extern __shared__ double2 sm[];
+  const int T = g.tile, Tp = g.tilep, nx = g.nx, nyz = g.nyz;
+  const int t0 = blockIdx.x * T;
+  const int b = blockIdx.y;
+  const int nt = min(T, nyz - t0);
+  if (IN == 0) {
+    if (a.nxin < nx) {
+      for (int i = threadIdx.x; i < nx * Tp; i += NT) sm[i] = make_double2(0.0, 0.0);
+      __syncthreads();
+    }
+    const double2* src = a.win + (size_t)b * a.in_stride;
+    for (int i = threadIdx.x; i < a.nxin * nt; i += NT) {
+      const int p = i / nt, t = i - p * nt;
+      sm[a.xin[p] * Tp + t] = src[(size_t)p * nyz + t0 + t];
+    }
+  } else {
+    const size_t base = (size_t)b * a.in_stride + (size_t)t0 * nx;
+    for (int i = threadIdx.x; i < nt * nx; i += NT) {
+      const int t = i / nx, x = i - t * nx;
+      sm[x * Tp + t] = (IN == 1) ? a.cin[base + i] : make_double2(a.rin[base + i], 0.0);
+    }
+  }
+  __syncthreads();
+  if (a.mode == 1) {
+    fft_lines<NT>(sm, g.px, nt, Tp, 1, nullptr, false);
+  } else if (a.mode >= 2) {
+    fft_lines<NT>(sm, g.px, nt, Tp, 1, nullptr, true);
+    if (a.mode == 3) {
+      const double* vv = a.v + (size_t)t0 * nx;
+      for (int i = threadIdx.x; i < nt * nx; i += NT) {
+        const int t = i / nx, x = i - t * nx;
+        sm[x * Tp + t] = cscale(sm[x * Tp + t], vv[i] * a.vscale);
+      }
+      __syncthreads();
+      fft_lines<NT>(sm, g.px, nt, Tp, 1, nullptr, false);
+    }
+  }
+  if (OUT == 0) {
+    double2* dst = a.wout + (size_t)b * a.out_stride;
+    for (int i = threadIdx.x; i < a.nxout * nt; i += NT) {
+      const int p = i / nt, t = i - p * nt;
+      dst[(size_t)p * nyz + t0 + t] = cscale(sm[a.xout[p] * Tp + t], a.oscale);
+    }
+  } else {
+    const size_t base = (size_t)b * a.out_stride + (size_t)t0 * nx;
+    for (int i = threadIdx.x; i < nt * nx; i += NT) {
+      const int t = i / nx, x = i - t * nx;
+      const double2 v = sm[x * Tp + t];
+      if (OUT == 1) {
+        a.cout[base + i] = cscale(v, a.oscale);
+      } else {
+        double r = v.x * a.oscale;
+        if (a.lda_v) {
+          const size_t gi = (size_t)t0 * nx + i;
+          const double rho = fmax(a.lda_rho[gi], 1e-10);
+          r += a.lda_c * pow(rho, -2.0 / 3.0) * a.lda_v[gi];
+        }
+        a.rout[base + i] = r;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// full plane pass on all y/z lines of Wf[v][x][z][y].
+//   mode 0: transform (forward: y then z; inverse: z then y)
+//   mode 1: Hartree  D = 4 pi / |G|^2 (0 at G = 0)     fwd -> *D -> inv
+//   mode 2: Kerker   D = |G|^2/(|G|^2+alpha^2) (1 at G=0)
+__global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restrict__ Wf, int mode,
+                                                   double param, int inverse) {
+  extern __shared__ double2 sm[];
+  const int x = blockIdx.x;
+  const int v = blockIdx.y;
+  const int nyz = g.nyz;
+  double2* pl = Wf + ((size_t)v * g.nx + x) * nyz;
+  for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = pl[i];
+  __syncthreads();
+  if (mode == 0 && inverse) {
+    fft_lines<NT>(sm, g.pz, g.ny, g.ny, 1, nullptr, true);
+    fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, true);
+  } else {
+    fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, false);
+    fft_lines<NT>(sm, g.pz, g.ny, g.ny, 1, nullptr, false);
+  }
+  if (mode != 0) {
+    const double* g2 = g.g2w + (size_t)x * nyz;
+    for (int i = threadIdx.x; i < nyz; i += NT) {
+      const double q = g2[i];
+      double d;
+      if (mode == 1) d = (q == 0.0) ? 0.0 : 4.0 * M_PI / q;
+      else d = (q == 0.0) ? 1.0 : q / (q + param * param);
+      sm[i] = cscale(sm[i], d);
+    }
+    __syncthreads();
+    fft_lines<NT>(sm, g.pz, g.ny, g.ny, 1, nullptr, true);
+    fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, true);
+  }
+  for (int i = threadIdx.x; i < nyz; i += NT) pl[i] = sm[i];
+}
+
+// ----------------------------------------------------------------------------
+size_t plane_smem(const pwb_grid* g) { return (size_t)g->nyz * sizeof(double2); }
+size_t pencil_smem(const pwb_grid* g) { return (size_t)g->nx * g->dev.tilep * sizeof(double2); }
+
+static int tiles(const pwb_grid* g) { return (g->nyz + g->dev.tile - 1) / g->dev.tile; }
+
+static int check_band_count(int n) {
+  if (n < 0 || n > 65535) return fail(PWB_ERR_VALUE, "band batch must be 0..65535 rows");
+  return PWB_OK;
+}
+
+int launch_plane_inv(pwb_grid* g, int nband, const int* band_k, const double2* psi, double scale,
+                     double2* W) {
+  PWB_TRY(check_band_count(nband));
+  if (nband == 0) return PWB_OK;
+  dim3 grid(g->nxa, nband);
+  k_plane_inv<<<grid, NT, plane_smem(g), g->stream>>>(g->dev, psi, nullptr, band_k, scale, W);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int launch_plane_inv2(pwb_grid* g, int nband, const int* band_k, const double2* a,
+                      const double2* b, double2* W) {
+  PWB_TRY(check_band_count(nband));
+  if (nband == 0) return PWB_OK;
+  dim3 grid(g->nxa, nband);
+  k_plane_inv<<<grid, NT, plane_smem(g), g->stream>>>(g->dev, a, b, band_k, 1.0, W);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int launch_plane_fwd(pwb_grid* g, int nband, const int* band_k, const double2* W, double a,
+                     const double2* psi_in, const double* shift, double2* out) {
+  PWB_TRY(check_band_count(nband));
+  if (nband == 0) return PWB_OK;
+  dim3 grid(g->nxa, nband);
+  k_plane_fwd<<<grid, NT, plane_smem(g), g->stream>>>(g->dev, W, band_k, a, psi_in, shift, out);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+static PencilArgs empty_args() {
+  PencilArgs a;
+  memset(&a, 0, sizeof(a));
+  a.vscale = 1.0;
+  a.oscale = 1.0;
+  return a;
+}
+
+int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, double vscale) {
+  PWB_TRY(check_band_count(nband));
+  if (nband == 0) return PWB_OK;
+  PencilArgs a = empty_args();
+  a.win = W;
+  a.xin = g->dev.xa;
+  a.nxin = g->nxa;
+  a.in_stride = (size_t)g->nxa * g->nyz;
+  a.v = v;
+  a.vscale = vscale;
+  a.mode = 3;
+  a.wout = W;
+  a.xout = g->dev.xa;
+  a.nxout = g->nxa;
+  a.out_stride = a.in_stride;
+  dim3 grid(tiles(g), nband);
+  k_pencil<0, 0><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int launch_pencil_to_cube(pwb_grid* g, int nband, const double2* W, double scale, double2* out) {
+  PWB_TRY(check_band_count(nband));
+  if (nband == 0) return PWB_OK;
+  PencilArgs a = empty_args();
+  a.win = W;
+  a.xin = g->dev.xa;
+  a.nxin = g->nxa;
+  a.in_stride = (size_t)g->nxa * g->nyz;
+  a.mode = 2;
+  a.cout = out;
+  a.out_stride = (size_t)g->ng;
+  a.oscale = scale;
+  dim3 grid(tiles(g), nband);
+  k_pencil<0, 1><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int launch_pencil_from_cube(pwb_grid* g, int nband, const double2* in, double2* W) {
+  PWB_TRY(check_band_count(nband));
+  if (nband == 0) return PWB_OK;
+  PencilArgs a = empty_args();
+  a.cin = in;
+  a.in_stride = (size_t)g->ng;
+  a.mode = 1;
+  a.wout = W;
+  a.xout = g->dev.xa;
+  a.nxout = g->nxa;
+  a.out_stride = (size_t)g->nxa * g->nyz;
+  dim3 grid(tiles(g), nband);
+  k_pencil<1, 0><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int launch_full_from_natural(pwb_grid* g, int nvec, const double2* in_c, const double* in_r,
+                             int mode, double2* Wf) {
+  PWB_TRY(check_band_count(nvec));
+  if (nvec == 0) return PWB_OK;
+  PencilArgs a = empty_args();
+  a.cin = in_c;
+  a.rin = in_r;
+  a.in_stride = (size_t)g->ng;
+  a.mode = mode;
+  a.wout = Wf;
+  a.xout = g->dev.xall;
+  a.nxout = g->nx;
+  a.out_stride = (size_t)g->ng;
+  dim3 grid(tiles(g), nvec);
+  if (in_c)
+    k_pencil<1, 0><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  else
+    k_pencil<2, 0><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int launch_full_plane(pwb_grid* g, int nvec, double2* Wf, int mode, double param, int inverse) {
+  PWB_TRY(check_band_count(nvec));
+  if (nvec == 0) return PWB_OK;
+  dim3 grid(g->nx, nvec);
+  k_plane_full<<<grid, NT, plane_smem(g), g->stream>>>(g->dev, Wf, mode, param, inverse);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int launch_full_to_natural(pwb_grid* g, int nvec, const double2* Wf, int mode, double scale,
+                           double2* out_c, double* out_r, const double* v_lda,
+                           const double* rho_lda) {
+  PWB_TRY(check_band_count(nvec));
+  if (nvec == 0) return PWB_OK;
+  PencilArgs a = empty_args();
+  a.win = Wf;
+  a.xin = g->dev.xall;
+  a.nxin = g->nx;
+  a.in_stride = (size_t)g->ng;
+  a.mode = mode;
+  a.cout = out_c;
+  a.rout = out_r;
+  a.out_stride = (size_t)g->ng;
+  a.oscale = scale;
+  a.lda_v = v_lda;
+  a.lda_rho = rho_lda;
+  a.lda_c = -(1.0 / 3.0) * cbrt(3.0 / M_PI);
+  dim3 grid(tiles(g), nvec);
+  if (out_c)
+    k_pencil<0, 1><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  else
+    k_pencil<0, 2><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int configure_kernels(const pwb_grid* g) {
+  const size_t ps = plane_smem(g), cs = pencil_smem(g);
+  if (ps > 227 * 1024 || cs > 227 * 1024)
+    return fail(PWB_ERR_UNSUPPORTED, "grid plane does not fit in shared memory");
+  PWB_CUDA(cudaFuncSetAttribute(k_plane_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps));
+  PWB_CUDA(cudaFuncSetAttribute(k_plane_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps));
+  PWB_CUDA(cudaFuncSetAttribute(k_plane_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps));
+  PWB_CUDA(cudaFuncSetAttribute(k_pencil<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+  PWB_CUDA(cudaFuncSetAttribute(k_pencil<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+  PWB_CUDA(cudaFuncSetAttribute(k_pencil<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+  PWB_CUDA(cudaFuncSetAttribute(k_pencil<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+  PWB_CUDA(cudaFuncSetAttribute(k_pencil<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+  return PWB_OK;
+}
+
+}  // namespace pwb

@@ -1,0 +1,41 @@
+// Projector GEMM plans (see proj.cu).
+#pragma once
+
+#include <algorithm>
+#include <vector>
+
+#include "grid.cuh"
+
+namespace pwb {
+
+struct ProjTile {
+  int row0;   // first row of X in this tile
+  int nrows;  // <= 32, all in k block `k`
+  int k;
+};
+
+struct ProjArgs {
+  const double2* phi;   // state orbital rows [nband][nbp]
+  const int* off;       // [nk] first orbital row of block k
+  const int* nocc;      // [nk]
+  const ProjTile* tiles;
+  int nbp;
+  int ldc;              // leading dim of C / partials (max nocc)
+  int nrows_total;
+};
+
+struct ProjPlan {
+  std::vector<ProjTile> tiles;
+  DevBuf dtiles;
+  int nrows = 0, mtiles = 0, nsplit = 1, split_len = 0;
+};
+
+int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int>& nocc, int nbp);
+// C = Phi^H X   (part: nsplit * nrows * ldc scratch)
+int proj_coeffs(const ProjPlan& pl, ProjArgs a, const double2* X, double2* part, double2* C,
+                cudaStream_t st);
+// Y = ca X + cb Phi C  (rows with active[row % band_mod] == 0 untouched; active may be NULL)
+int proj_apply(const ProjPlan& pl, ProjArgs a, const double2* C, const double2* Xin, double2* Y,
+               double ca, double cb, const int* active, int band_mod, cudaStream_t st);
+
+}  // namespace pwb

@@ -1,0 +1,765 @@
+// Device ground state, batched projected Sternheimer PCG, and the chi0 driver.
+//
+// Reference semantics kept exactly (sternheimer.py:33-98, response.py:110-161):
+//   x = 0, r = rhs, z = Q(M^-1 r), p = z, rz = Re<r,z>
+//   loop: p = Qp; Ap = Q(Hp - eps p); it++; a = rz/Re<p,Ap> (0 if <= 0);
+//         x += a p; r -= a Ap; x = Qx; r = Qr; |r| <= tol -> stop;
+//         it >= max_iter -> NonConvergence; z = Q(M^-1 r);
+//         b = rz'/rz (0 if rz == 0); p = z + b p
+// for every (k, n) row of the batch at once.  Converged rows are masked: their
+// x, r, iteration count and residual are frozen exactly where the reference
+// loop would have returned, while the remaining rows keep iterating.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "state.cuh"
+
+namespace pwb {
+
+int configure_chi0_kernels(const pwb_grid* g);
+
+constexpr int NTC = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NTC / 32; ++i) s += red[i];
+    red[NTC / 32] = s;
+  }
+  __syncthreads();
+  return red[NTC / 32];
+}
+
+// minv_s = 1 / (kin_s + pshift)
+__device__ __forceinline__ double minv(const GridDev& g, int k, int s, double pshift) {
+  return 1.0 / (g.kin[(size_t)k * g.nbp + s] + pshift);
+}
+
+// x = 0, r = rhs, z = M^-1 r
+__global__ void __launch_bounds__(NTC) k_cg_init(GridDev g, CgScalars sc, int n,
+                                                 const double2* __restrict__ rhs,
+                                                 double2* __restrict__ xr, double2* __restrict__ z) {
+  const int row = blockIdx.x;
+  const int k = sc.row_k[row];
+  const double ps = sc.pshift[row];
+  double2* x = xr + (size_t)row * g.nbp;
+  double2* r = xr + (size_t)(n + row) * g.nbp;
+  double2* zz = z + (size_t)row * g.nbp;
+  const double2* b = rhs + (size_t)row * g.nbp;
+  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
+    const double2 v = b[s];
+    x[s] = make_double2(0.0, 0.0);
+    r[s] = v;
+    zz[s] = cscale(v, minv(g, k, s, ps));
+  }
+  if (threadIdx.x == 0) {
+    sc.active[row] = 1;
+    sc.iters[row] = 0;
+    sc.res[row] = 0.0;
+  }
+}
+
+// rz = Re<r, z>; p = z
+__global__ void __launch_bounds__(NTC) k_cg_init2(GridDev g, CgScalars sc, int n,
+                                                  const double2* __restrict__ xr,
+                                                  const double2* __restrict__ z,
+                                                  double2* __restrict__ p) {
+  __shared__ double red[NTC / 32 + 1];
+  const int row = blockIdx.x;
+  const double2* r = xr + (size_t)(n + row) * g.nbp;
+  const double2* zz = z + (size_t)row * g.nbp;
+  double2* pp = p + (size_t)row * g.nbp;
+  double acc = 0.0;
+  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
+    const double2 a = r[s], c = zz[s];
+    acc += a.x * c.x + a.y * c.y;
+    pp[s] = c;
+  }
+  const double rz = block_sum(acc, red);
+  if (threadIdx.x == 0) sc.rz[row] = rz;
+}
+
+// alpha = rz / Re<p, Ap> (0 if <= 0); x += alpha p; r -= alpha Ap   (active rows)
+__global__ void __launch_bounds__(NTC) k_cg_alpha(GridDev g, CgScalars sc, int n,
+                                                  const double2* __restrict__ p,
+                                                  const double2* __restrict__ ap,
+                                                  double2* __restrict__ xr) {
+  __shared__ double red[NTC / 32 + 1];
+  const int row = blockIdx.x;
+  if (!sc.active[row]) return;
+  const double2* pp = p + (size_t)row * g.nbp;
+  const double2* aa = ap + (size_t)row * g.nbp;
+  double acc = 0.0;
+  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
+    const double2 a = pp[s], c = aa[s];
+    acc += a.x * c.x + a.y * c.y;
+  }
+  const double pap = block_sum(acc, red);
+  const double alpha = pap > 0.0 ? sc.rz[row] / pap : 0.0;
+  double2* x = xr + (size_t)row * g.nbp;
+  double2* r = xr + (size_t)(n + row) * g.nbp;
+  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
+    const double2 a = pp[s], c = aa[s];
+    double2 xv = x[s], rv = r[s];
+    xv.x += alpha * a.x;
+    xv.y += alpha * a.y;
+    rv.x -= alpha * c.x;
+    rv.y -= alpha * c.y;
+    x[s] = xv;
+    r[s] = rv;
+  }
+}
+
+// res = |r|; it++; converged / failed masking; z = M^-1 r for rows still active
+__global__ void __launch_bounds__(NTC) k_cg_resid(GridDev g, CgScalars sc, int n,
+                                                  const double2* __restrict__ xr,
+                                                  double2* __restrict__ z) {
+  __shared__ double red[NTC / 32 + 1];
+  const int row = blockIdx.x;
+  if (!sc.active[row]) return;
+  const double2* r = xr + (size_t)(n + row) * g.nbp;
+  double acc = 0.0;
+  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
+    const double2 a = r[s];
+    acc += a.x * a.x + a.y * a.y;
+  }
+  const double res = sqrt(block_sum(acc, red));
+  const int it = sc.iters[row] + 1;
+  bool done = res <= sc.tol[row];
+  bool failed = !done && it >= sc.maxit[row];
+  if (threadIdx.x == 0) {
+    sc.res[row] = res;
+    sc.iters[row] = it;
+    if (done || failed) sc.active[row] = 0;
+    if (failed) atomicExch(&sc.counters[1], 1);
+    if (!done && !failed) atomicAdd(&sc.counters[0], 1);
+  }
+  if (done || failed) return;
+  const int k = sc.row_k[row];
+  const double ps = sc.pshift[row];
+  double2* zz = z + (size_t)row * g.nbp;
+  for (int s = threadIdx.x; s < g.nbp; s += NTC) zz[s] = cscale(r[s], minv(g, k, s, ps));
+}
+
+// rz' = Re<r, z>; beta = rz'/rz (0 if rz == 0); rz = rz'; p = z + beta p
+__global__ void __launch_bounds__(NTC) k_cg_beta(GridDev g, CgScalars sc, int n,
+                                                 const double2* __restrict__ xr,
+                                                 const double2* __restrict__ z,
+                                                 double2* __restrict__ p) {
+  __shared__ double red[NTC / 32 + 1];
+  const int row = blockIdx.x;
+  if (!sc.active[row]) return;
+  const double2* r = xr + (size_t)(n + row) * g.nbp;
+  const double2* zz = z + (size_t)row * g.nbp;
+  double acc = 0.0;
+  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
+    const double2 a = r[s], c = zz[s];
+    acc += a.x * c.x + a.y * c.y;
+  }
+  const double rzn = block_sum(acc, red);
+  const double rz = sc.rz[row];
+  const double beta = rz != 0.0 ? rzn / rz : 0.0;
+  double2* pp = p + (size_t)row * g.nbp;
+  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
+    const double2 c = zz[s], q = pp[s];
+    pp[s] = make_double2(c.x + beta * q.x, c.y + beta * q.y);
+  }
+  if (threadIdx.x == 0) sc.rz[row] = rzn;
+}
+
+__global__ void k_zero_counters(int* c) {
+  c[0] = 0;
+  c[1] = 0;
+}
+
+// ---- chi0 helpers --------------------------------------------------------------
+// delta eps of local rows; fsum = sum w_k f'_n delta eps_n (fixed order, 1 CTA)
+__global__ void k_chi0_eps(int r0, int nrows, int ldc, const int* __restrict__ band_k,
+                           const int* __restrict__ off, const double2* __restrict__ C,
+                           const double* __restrict__ coef, double* __restrict__ deps,
+                           double* __restrict__ fsum) {
+  // coef layout per band: [0] w*2f/sqrt(Omega), [1] w*f', [2] f', [3] w
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nrows; i += 256) {
+    const int band = r0 + i;
+    const int n = band - off[band_k[band]];
+    const double de = C[(size_t)i * ldc + n].x;
+    deps[i] = de;
+    acc += coef[4 * band + 1] * de;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) fsum[0] = red[0];
+}
+
+// delta f, accumulation weights, and Cw = W o M for the occupied pair term
+__global__ void k_chi0_occ(int r0, int nrows, int ldc, const int* __restrict__ band_k,
+                           const int* __restrict__ nocc, const double* __restrict__ coef,
+                           const double* __restrict__ fsum, double den, double thresh,
+                           const double* __restrict__ deps, const double* __restrict__ wt,
+                           const double2* __restrict__ C, double2* __restrict__ Cw,
+                           double* __restrict__ c2, double* __restrict__ c1) {
+  const int i = blockIdx.x;
+  const int band = r0 + i;
+  const double def = (fabs(den) > thresh) ? fsum[0] / den : 0.0;
+  const int no = nocc[band_k[band]];
+  for (int m = threadIdx.x; m < ldc; m += blockDim.x) {
+    const double w = (m < no) ? wt[(size_t)band * ldc + m] : 0.0;
+    Cw[(size_t)i * ldc + m] = cscale(C[(size_t)i * ldc + m], w);
+  }
+  if (threadIdx.x == 0) {
+    const double df = coef[4 * band + 2] * (deps[i] - def);
+    c2[i] = coef[4 * band + 0];
+    c1[i] = coef[4 * band + 3] * df;
+  }
+}
+
+static int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands) {
+  pwb_grid* g = st->g;
+  const int n = (int)bands.size();
+  if (cg.nrows == n && cg.bands == bands) return PWB_OK;
+  cg.nrows = n;
+  cg.bands = bands;
+  std::vector<int> rk(n), rk2(2 * n);
+  for (int i = 0; i < n; ++i) {
+    if (bands[i] < 0 || bands[i] >= st->nband) return fail(PWB_ERR_VALUE, "band index out of range");
+    rk[i] = st->band_k[bands[i]];
+    rk2[i] = rk2[n + i] = rk[i];
+  }
+  PWB_TRY(proj_plan(cg.plan1, rk, st->nocc, g->nbp));
+  PWB_TRY(proj_plan(cg.plan2, rk2, st->nocc, g->nbp));
+  const size_t row = (size_t)g->nbp * sizeof(double2);
+  PWB_TRY(cg.xr.ensure(2 * n * row));
+  PWB_TRY(cg.z.ensure(n * row));
+  PWB_TRY(cg.p.ensure(n * row));
+  PWB_TRY(cg.ap.ensure(n * row));
+  PWB_TRY(cg.rhs.ensure(n * row));
+  PWB_CUDA(cudaMemset(cg.ap.ptr, 0, n * row));
+  PWB_CUDA(cudaMemset(cg.z.ptr, 0, n * row));
+  const int nsp = std::max(cg.plan1.nsplit, cg.plan2.nsplit);
+  PWB_TRY(cg.part.ensure((size_t)nsp * 2 * n * st->ldc * sizeof(double2)));
+  PWB_TRY(cg.cmat.ensure((size_t)2 * n * st->ldc * sizeof(double2)));
+  // scalars
+  const size_t nd = 5 * (size_t)n, ni = 4 * (size_t)n + 2;
+  PWB_TRY(cg.scal.ensure(nd * sizeof(double) + ni * sizeof(int)));
+  double* d = as<double>(cg.scal);
+  cg.s.rz = d;
+  cg.s.res = d + n;
+  cg.s.tol = d + 2 * n;
+  cg.s.eps = d + 3 * n;
+  cg.s.pshift = d + 4 * n;
+  int* ip = reinterpret_cast<int*>(d + nd);
+  cg.s.active = ip;
+  cg.s.iters = ip + n;
+  cg.s.maxit = ip + 2 * n;
+  cg.s.row_k = ip + 3 * n;
+  cg.s.counters = ip + 4 * n;
+  std::vector<double> eps(n), ps(n);
+  for (int i = 0; i < n; ++i) {
+    eps[i] = st->eps[bands[i]];
+    ps[i] = std::max(eps[i], 0.1);   // PRECONDITIONER_SHIFT_FLOOR (sternheimer.py:19)
+  }
+  PWB_CUDA(cudaMemcpy(cg.s.eps, eps.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  PWB_CUDA(cudaMemcpy(cg.s.pshift, ps.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  PWB_CUDA(cudaMemcpy(cg.s.row_k, rk.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+  if (!cg.h_counters) PWB_CUDA(cudaMallocHost(&cg.h_counters, 2 * sizeof(int)));
+  return PWB_OK;
+}
+
+static ProjArgs proj_args(pwb_state* st) {
+  ProjArgs a;
+  a.phi = as<double2>(st->phi);
+  a.off = as<int>(st->d_off);
+  a.nocc = as<int>(st->d_nocc);
+  a.tiles = nullptr;
+  a.nbp = st->g->nbp;
+  a.ldc = st->ldc;
+  a.nrows_total = 0;
+  return a;
+}
+
+// Q X in place for rows of a plan (masked)
+static int project(pwb_state* st, CgBatch& cg, const ProjPlan& pl, double2* X, const int* active,
+                   int band_mod) {
+  ProjArgs a = proj_args(st);
+  cudaStream_t s = st->g->stream;
+  PWB_TRY(proj_coeffs(pl, a, X, as<double2>(cg.part), as<double2>(cg.cmat), s));
+  PWB_TRY(proj_apply(pl, a, as<double2>(cg.cmat), X, X, 1.0, -1.0, active, band_mod, s));
+  return PWB_OK;
+}
+
+// Run the batched PCG on cg.rhs with tolerances already in cg.s.tol.
+// On return x = rows [0, n) of cg.xr.
+static int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max_iter,
+                    int* iters_host, double* res_host) {
+  pwb_grid* g = st->g;
+  cudaStream_t s = g->stream;
+  const int n = cg.nrows;
+  if (n == 0) return PWB_OK;
+  std::vector<int> maxit(n);
+  for (int i = 0; i < n; ++i)
+    maxit[i] = max_iter > 0 ? max_iter : 10 * g->nb[st->band_k[cg.bands[i]]];
+  PWB_CUDA(cudaMemcpyAsync(cg.s.tol, tol.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+  PWB_CUDA(cudaMemcpyAsync(cg.s.maxit, maxit.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
+  double2* xr = as<double2>(cg.xr);
+  double2* z = as<double2>(cg.z);
+  double2* p = as<double2>(cg.p);
+  double2* ap = as<double2>(cg.ap);
+  const int* bk = cg.s.row_k;
+  k_cg_init<<<n, NTC, 0, s>>>(g->dev, cg.s, n, as<double2>(cg.rhs), xr, z);
+  PWB_LAUNCH_CHECK();
+  PWB_TRY(project(st, cg, cg.plan1, z, nullptr, n));
+  k_cg_init2<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, p);
+  PWB_LAUNCH_CHECK();
+  PWB_TRY(g->wbuf.ensure((size_t)n * g->nxa * g->nyz * sizeof(double2)));
+  double2* W = as<double2>(g->wbuf);
+  const double* vloc = as<double>(st->vloc);
+  bool failed = false;
+  for (int it = 0;; ++it) {
+    PWB_TRY(project(st, cg, cg.plan1, p, cg.s.active, n));
+    PWB_TRY(launch_plane_inv(g, n, bk, p, 1.0, W));
+    PWB_TRY(launch_pencil_vmul(g, n, W, vloc, 1.0 / g->ng));
+    PWB_TRY(launch_plane_fwd(g, n, bk, W, 1.0, p, cg.s.eps, ap));
+    PWB_TRY(project(st, cg, cg.plan1, ap, cg.s.active, n));
+    k_cg_alpha<<<n, NTC, 0, s>>>(g->dev, cg.s, n, p, ap, xr);
+    PWB_LAUNCH_CHECK();
+    PWB_TRY(project(st, cg, cg.plan2, xr, cg.s.active, n));
+    k_zero_counters<<<1, 1, 0, s>>>(cg.s.counters);
+    PWB_LAUNCH_CHECK();
+    k_cg_resid<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z);
+    PWB_LAUNCH_CHECK();
+    PWB_CUDA(cudaMemcpyAsync(cg.h_counters, cg.s.counters, 2 * sizeof(int),
+                             cudaMemcpyDeviceToHost, s));
+    PWB_TRY(project(st, cg, cg.plan1, z, cg.s.active, n));
+    k_cg_beta<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, p);
+    PWB_LAUNCH_CHECK();
+    PWB_CUDA(cudaStreamSynchronize(s));
+    if (cg.h_counters[1]) failed = true;
+    if (cg.h_counters[0] == 0) break;
+  }
+  std::vector<int> its(n);
+  std::vector<double> res(n);
+  PWB_CUDA(cudaMemcpyAsync(its.data(), cg.s.iters, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+  PWB_CUDA(cudaMemcpyAsync(res.data(), cg.s.res, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  PWB_CUDA(cudaStreamSynchronize(s));
+  int first_fail = -1;
+  for (int i = 0; i < n; ++i) {
+    if (res[i] > tol[i]) {
+      if (first_fail < 0) first_fail = i;
+      its[i] = -1;
+    }
+    if (iters_host) iters_host[i] = its[i];
+    if (res_host) res_host[i] = res[i];
+  }
+  if (failed || first_fail >= 0) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "Sternheimer CG for band %d stalled at %.3e (target %.3e)",
+             first_fail >= 0 ? cg.bands[first_fail] : -1,
+             first_fail >= 0 ? res[first_fail] : 0.0, first_fail >= 0 ? tol[first_fail] : 0.0);
+    return fail(PWB_ERR_NONCONV, buf);
+  }
+  return PWB_OK;
+}
+
+// psi(r) cache for rows [b0, b1)
+static int ensure_psir(pwb_state* st, int b0, int b1) {
+  if (st->psir_b0 == b0 && st->psir_b1 == b1) return PWB_OK;
+  pwb_grid* g = st->g;
+  const int n = b1 - b0;
+  PWB_TRY(st->psir.ensure((size_t)std::max(n, 1) * g->ng * sizeof(double2)));
+  PWB_TRY(g->wbuf.ensure((size_t)std::max(n, 1) * g->nxa * g->nyz * sizeof(double2)));
+  double2* W = as<double2>(g->wbuf);
+  const double2* phi = as<double2>(st->phi) + (size_t)b0 * g->nbp;
+  const int* bk = as<int>(st->d_band_k) + b0;
+  PWB_TRY(launch_plane_inv(g, n, bk, phi, 1.0, W));
+  PWB_TRY(launch_pencil_to_cube(g, n, W, 1.0 / std::sqrt(g->volume), as<double2>(st->psir)));
+  st->psir_b0 = b0;
+  st->psir_b1 = b1;
+  return PWB_OK;
+}
+
+}  // namespace pwb
+
+using namespace pwb;
+
+extern "C" {
+
+int pwb_state_create(pwb_grid* g, const int* nocc_per_k, const double* kweight,
+                     const double* phi, const double* eps, const double* occ,
+                     const double* fprime, const double* v_local, const double* rho,
+                     pwb_state** out) {
+  if (!g || !out) return fail(PWB_ERR_VALUE, "null argument");
+  *out = nullptr;
+  std::unique_ptr<pwb_state> st(new pwb_state());
+  st->g = g;
+  st->nk = g->nk;
+  st->nocc.assign(nocc_per_k, nocc_per_k + g->nk);
+  st->w.assign(kweight, kweight + g->nk);
+  st->off.resize(g->nk);
+  int nb = 0, ldc = 0;
+  for (int k = 0; k < g->nk; ++k) {
+    if (st->nocc[k] < 1 || st->nocc[k] > g->nb[k])
+      return fail(PWB_ERR_VALUE, "n_occ must lie in 1..n_b for every k");
+    st->off[k] = nb;
+    nb += st->nocc[k];
+    ldc = std::max(ldc, st->nocc[k]);
+  }
+  st->nband = nb;
+  st->ldc = ldc;
+  st->eps.assign(eps, eps + nb);
+  st->occ.assign(occ, occ + nb);
+  st->fprime.assign(fprime, fprime + nb);
+  st->band_k.resize(nb);
+  double den = 0.0, thr = 0.0;
+  for (int k = 0; k < g->nk; ++k) {
+    for (int n = 0; n < st->nocc[k]; ++n) {
+      st->band_k[st->off[k] + n] = k;
+      den += st->w[k] * st->fprime[st->off[k] + n];
+    }
+    thr += st->w[k] * st->nocc[k];
+  }
+  st->fp_den = den;
+  st->fp_thresh = 1e-14 * thr;   // response.py:135 (abs(fp_sum) > 1e-14 * n_occ)
+
+  // orbitals -> padded rows
+  const size_t row = (size_t)g->nbp;
+  std::vector<double2> hphi((size_t)nb * row, make_double2(0.0, 0.0));
+  const double2* src = reinterpret_cast<const double2*>(phi);
+  size_t so = 0;
+  for (int k = 0; k < g->nk; ++k)
+    for (int n = 0; n < st->nocc[k]; ++n) {
+      memcpy(&hphi[(size_t)(st->off[k] + n) * row], src + so, g->nb[k] * sizeof(double2));
+      so += g->nb[k];
+    }
+  PWB_TRY(st->phi.ensure(hphi.size() * sizeof(double2)));
+  PWB_CUDA(cudaMemcpy(st->phi.ptr, hphi.data(), hphi.size() * sizeof(double2),
+                      cudaMemcpyHostToDevice));
+  PWB_TRY(st->d_off.ensure(g->nk * sizeof(int)));
+  PWB_TRY(st->d_nocc.ensure(g->nk * sizeof(int)));
+  PWB_TRY(st->d_band_k.ensure(nb * sizeof(int)));
+  PWB_CUDA(cudaMemcpy(st->d_off.ptr, st->off.data(), g->nk * sizeof(int), cudaMemcpyHostToDevice));
+  PWB_CUDA(cudaMemcpy(st->d_nocc.ptr, st->nocc.data(), g->nk * sizeof(int), cudaMemcpyHostToDevice));
+  PWB_CUDA(cudaMemcpy(st->d_band_k.ptr, st->band_k.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
+
+  // per-band coefficients [w*2f/sqrt(Omega), w*f', f', w]
+  std::vector<double> coef(4 * (size_t)nb);
+  const double isv = 1.0 / std::sqrt(g->volume);
+  for (int b = 0; b < nb; ++b) {
+    const double w = st->w[st->band_k[b]];
+    coef[4 * b + 0] = w * 2.0 * st->occ[b] * isv;
+    coef[4 * b + 1] = w * st->fprime[b];
+    coef[4 * b + 2] = st->fprime[b];
+    coef[4 * b + 3] = w;
+  }
+  PWB_TRY(st->d_coef.ensure(coef.size() * sizeof(double)));
+  PWB_CUDA(cudaMemcpy(st->d_coef.ptr, coef.data(), coef.size() * sizeof(double),
+                      cudaMemcpyHostToDevice));
+  // occupied pair weights, stored transposed: wt[band n][m] = W[m][n] (response.py:74-98)
+  std::vector<double> wt((size_t)nb * ldc, 0.0);
+  for (int k = 0; k < g->nk; ++k) {
+    const int o = st->off[k], no = st->nocc[k];
+    for (int n = 0; n < no; ++n)
+      for (int m = 0; m < no; ++m) {
+        if (m == n) continue;
+        const double en = st->eps[o + n], em = st->eps[o + m];
+        const double fn = st->occ[o + n], fm = st->occ[o + m];
+        const double de = en - em;
+        const bool degen = std::fabs(de) <= 1e-8 * std::max(1.0, std::fabs(en));
+        const double ratio = degen ? st->fprime[o + n] : (fn - fm) / de;
+        wt[(size_t)(o + n) * ldc + m] = ratio * fn / (fn * fn + fm * fm);
+      }
+  }
+  PWB_TRY(st->wt.ensure(wt.size() * sizeof(double)));
+  PWB_CUDA(cudaMemcpy(st->wt.ptr, wt.data(), wt.size() * sizeof(double), cudaMemcpyHostToDevice));
+  PWB_TRY(st->vloc.ensure((size_t)g->ng * sizeof(double)));
+  PWB_TRY(st->rho.ensure((size_t)g->ng * sizeof(double)));
+  PWB_CUDA(cudaMemcpy(st->vloc.ptr, v_local, (size_t)g->ng * sizeof(double), cudaMemcpyHostToDevice));
+  if (rho)
+    PWB_CUDA(cudaMemcpy(st->rho.ptr, rho, (size_t)g->ng * sizeof(double), cudaMemcpyHostToDevice));
+  else
+    PWB_CUDA(cudaMemset(st->rho.ptr, 0, (size_t)g->ng * sizeof(double)));
+  PWB_TRY(configure_chi0_kernels(g));
+  *out = st.release();
+  return PWB_OK;
+}
+
+int pwb_state_destroy(pwb_state* st) {
+  if (!st) return PWB_OK;
+  cudaDeviceSynchronize();
+  if (st->cg.h_counters) cudaFreeHost(st->cg.h_counters);
+  if (st->cg_user.h_counters) cudaFreeHost(st->cg_user.h_counters);
+  delete st;
+  return PWB_OK;
+}
+
+int pwb_state_nbands(const pwb_state* st, int* nbands) {
+  if (!st || !nbands) return fail(PWB_ERR_VALUE, "null argument");
+  *nbands = st->nband;
+  return PWB_OK;
+}
+
+int pwb_project_out(pwb_state* st, int k, int ncol, double* x) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  if (k < 0 || k >= st->nk) return fail(PWB_ERR_VALUE, "k block out of range");
+  if (ncol <= 0) return PWB_OK;
+  std::vector<int> key(ncol, k);
+  if (st->user_plan_key != key) {
+    PWB_TRY(proj_plan(st->user_plan, key, st->nocc, st->g->nbp));
+    st->user_plan_key = key;
+  }
+  CgBatch& cg = st->cg_user;
+  PWB_TRY(cg.part.ensure((size_t)st->user_plan.nsplit * ncol * st->ldc * sizeof(double2)));
+  PWB_TRY(cg.cmat.ensure((size_t)ncol * st->ldc * sizeof(double2)));
+  return project(st, cg, st->user_plan, reinterpret_cast<double2*>(x), nullptr, ncol);
+}
+
+int pwb_sternheimer(pwb_state* st, int nrhs, const int* band_host, const double* rhs,
+                    const double* tol_host, int max_iter, double* x, int* iters_host,
+                    double* res_host) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  if (nrhs <= 0) return PWB_OK;
+  std::vector<int> bands(band_host, band_host + nrhs);
+  std::vector<double> tol(tol_host, tol_host + nrhs);
+  CgBatch& cg = st->cg_user;
+  PWB_TRY(cg_setup(st, cg, bands));
+  const size_t row = (size_t)st->g->nbp * sizeof(double2);
+  PWB_CUDA(cudaMemcpyAsync(cg.rhs.ptr, rhs, nrhs * row, cudaMemcpyDeviceToDevice, st->g->stream));
+  int status = cg_solve(st, cg, tol, max_iter, iters_host, res_host);
+  PWB_CUDA(cudaMemcpyAsync(x, cg.xr.ptr, nrhs * row, cudaMemcpyDeviceToDevice, st->g->stream));
+  PWB_CUDA(cudaStreamSynchronize(st->g->stream));
+  return status;
+}
+
+int pwb_chi0_begin(pwb_state* st, int b0, int b1, const double* dv, double* fsum) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  if (b0 < 0 || b1 > st->nband || b0 > b1) return fail(PWB_ERR_VALUE, "bad band range");
+  pwb_grid* g = st->g;
+  cudaStream_t s = g->stream;
+  const int n = b1 - b0;
+  st->shard_b0 = b0;
+  st->shard_b1 = b1;
+  std::vector<int> bands(n);
+  for (int i = 0; i < n; ++i) bands[i] = b0 + i;
+  PWB_TRY(cg_setup(st, st->cg, bands));
+  PWB_TRY(ensure_psir(st, b0, b1));
+  const size_t row = (size_t)g->nbp * sizeof(double2);
+  PWB_TRY(st->dvpsi.ensure(std::max(n, 1) * row));
+  PWB_TRY(st->dphi.ensure(std::max(n, 1) * row));
+  PWB_TRY(st->cm.ensure((size_t)std::max(n, 1) * st->ldc * sizeof(double2)));
+  PWB_TRY(st->cw.ensure((size_t)std::max(n, 1) * st->ldc * sizeof(double2)));
+  PWB_TRY(st->scal.ensure((size_t)(3 * std::max(n, 1) + 8) * sizeof(double)));
+  if (n == 0) {
+    PWB_CUDA(cudaMemsetAsync(fsum, 0, sizeof(double), s));
+    return PWB_OK;
+  }
+  PWB_CUDA(cudaMemsetAsync(st->dvpsi.ptr, 0, n * row, s));
+  PWB_CUDA(cudaMemsetAsync(st->dphi.ptr, 0, n * row, s));
+  // RHS: dvpsi = to_fourier(dv * to_real(phi_n))  (response.py:127-128)
+  PWB_TRY(g->wbuf.ensure((size_t)n * g->nxa * g->nyz * sizeof(double2)));
+  double2* W = as<double2>(g->wbuf);
+  const double2* phi = as<double2>(st->phi) + (size_t)b0 * g->nbp;
+  const int* bk = as<int>(st->d_band_k) + b0;
+  double2* dvpsi = as<double2>(st->dvpsi);
+  PWB_TRY(launch_plane_inv(g, n, bk, phi, 1.0, W));
+  PWB_TRY(launch_pencil_vmul(g, n, W, dv, 1.0 / g->ng));
+  PWB_TRY(launch_plane_fwd(g, n, bk, W, 1.0, nullptr, nullptr, dvpsi));
+  // M^T = (Phi^H dvpsi)^T  (response.py:129)
+  ProjArgs a = proj_args(st);
+  CgBatch& cg = st->cg;
+  PWB_TRY(proj_coeffs(cg.plan1, a, dvpsi, as<double2>(cg.part), as<double2>(st->cm), s));
+  double* deps = as<double>(st->scal);
+  k_chi0_eps<<<1, 256, 0, s>>>(b0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_off),
+                               as<double2>(st->cm), as<double>(st->d_coef), deps, fsum);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, double* drho,
+                    int* iters_host) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  pwb_grid* g = st->g;
+  cudaStream_t s = g->stream;
+  const int b0 = st->shard_b0, b1 = st->shard_b1, n = b1 - b0;
+  if (n == 0) {
+    PWB_CUDA(cudaMemsetAsync(drho, 0, (size_t)g->ng * sizeof(double), s));
+    PWB_CUDA(cudaStreamSynchronize(s));
+    return PWB_OK;
+  }
+  CgBatch& cg = st->cg;
+  double* deps = as<double>(st->scal);
+  double* c2 = deps + n;
+  double* c1 = deps + 2 * n;
+  ProjArgs a = proj_args(st);
+  k_chi0_occ<<<n, 64, 0, s>>>(b0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_nocc),
+                              as<double>(st->d_coef), fsum, st->fp_den, st->fp_thresh, deps,
+                              as<double>(st->wt), as<double2>(st->cm), as<double2>(st->cw), c2,
+                              c1);
+  PWB_LAUNCH_CHECK();
+  // delta phi^P = Phi (W o M)  (response.py:138)
+  PWB_TRY(proj_apply(cg.plan1, a, as<double2>(st->cw), nullptr, as<double2>(st->dphi), 0.0, 1.0,
+                     nullptr, n, s));
+  // rhs = -Q dvpsi (response.py:141), reusing Phi^H dvpsi
+  PWB_TRY(proj_apply(cg.plan1, a, as<double2>(st->cm), as<double2>(st->dvpsi),
+                     as<double2>(cg.rhs), -1.0, 1.0, nullptr, n, s));
+  std::vector<double> tol(tol_host, tol_host + n);
+  PWB_TRY(cg_solve(st, cg, tol, -1, iters_host, nullptr));
+  // drho accumulation (response.py:150-154)
+  double2* W = as<double2>(g->wbuf);
+  const int* bk = as<int>(st->d_band_k) + b0;
+  PWB_TRY(launch_plane_inv2(g, n, bk, as<double2>(st->dphi), as<double2>(cg.xr), W));
+  const int ntile = (g->nyz + g->dev.tile - 1) / g->dev.tile;
+  int nchunk = std::max(1, std::min(n, (2 * kSM + ntile - 1) / ntile));
+  PWB_TRY(st->drho_part.ensure((size_t)nchunk * g->ng * sizeof(double)));
+  PWB_TRY(launch_drho_partial(g, n, W, as<double2>(st->psir), c2, c1, nchunk,
+                              as<double>(st->drho_part)));
+  PWB_TRY(launch_drho_reduce(g, nchunk, as<double>(st->drho_part), drho));
+  PWB_CUDA(cudaStreamSynchronize(s));
+  return PWB_OK;
+}
+
+int pwb_chi0(pwb_state* st, const double* dv, const double* tol_host, double* drho,
+             int* iters_host) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  PWB_TRY(st->fsum.ensure(2 * sizeof(double)));
+  PWB_TRY(pwb_chi0_begin(st, 0, st->nband, dv, as<double>(st->fsum)));
+  return pwb_chi0_finish(st, as<double>(st->fsum), tol_host, drho, iters_host);
+}
+
+int pwb_chi0_host(pwb_state* st, const double* dv_host, const double* tol_host,
+                  double* drho_host, int* iters_host) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  pwb_grid* g = st->g;
+  PWB_TRY(g->tmp_real.ensure((size_t)2 * g->ng * sizeof(double)));
+  double* ddv = as<double>(g->tmp_real);
+  double* ddr = ddv + g->ng;
+  PWB_CUDA(cudaMemcpyAsync(ddv, dv_host, (size_t)g->ng * sizeof(double), cudaMemcpyHostToDevice,
+                           g->stream));
+  PWB_TRY(pwb_chi0(st, ddv, tol_host, ddr, iters_host));
+  PWB_CUDA(cudaMemcpyAsync(drho_host, ddr, (size_t)g->ng * sizeof(double), cudaMemcpyDeviceToHost,
+                           g->stream));
+  PWB_CUDA(cudaStreamSynchronize(g->stream));
+  return PWB_OK;
+}
+
+int pwb_row_norm(pwb_state* st, int k, int real_part, double* out_host) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  if (k < 0 || k >= st->nk) return fail(PWB_ERR_VALUE, "k block out of range");
+  pwb_grid* g = st->g;
+  const int b0 = st->off[k], n = st->nocc[k];
+  DevBuf cache, res;
+  PWB_TRY(cache.ensure((size_t)n * g->ng * sizeof(double2)));
+  PWB_TRY(res.ensure(sizeof(double)));
+  PWB_TRY(g->wbuf.ensure((size_t)n * g->nxa * g->nyz * sizeof(double2)));
+  double2* W = as<double2>(g->wbuf);
+  PWB_TRY(launch_plane_inv(g, n, as<int>(st->d_band_k) + b0, as<double2>(st->phi) + (size_t)b0 * g->nbp,
+                           1.0, W));
+  PWB_TRY(launch_pencil_to_cube(g, n, W, 1.0 / std::sqrt(g->volume), as<double2>(cache)));
+  PWB_TRY(launch_row_norm(g, n, as<double2>(cache), real_part, as<double>(res)));
+  double v = 0.0;
+  PWB_CUDA(cudaMemcpyAsync(&v, res.ptr, sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+  PWB_CUDA(cudaStreamSynchronize(g->stream));
+  *out_host = std::sqrt(v);
+  return PWB_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Q X = X - Phi (Phi^H X) for an arbitrary orthonormal block (no state):
+// phi: nocc device rows of length nb; x: ncol device rows of length nb.
+int pwb_project_generic(int nb, int nocc, const double* phi, int ncol, double* x) {
+  if (nb < 1 || nocc < 1 || ncol < 0) return fail(PWB_ERR_VALUE, "bad projector sizes");
+  if (ncol == 0) return PWB_OK;
+  static thread_local ProjPlan plan;
+  static thread_local DevBuf part, cmat, meta;
+  static thread_local std::vector<int> key;
+  std::vector<int> rk(ncol, 0), nocc_v(1, nocc);
+  std::vector<int> k2 = {nb, nocc, ncol};
+  if (key != k2) {
+    PWB_TRY(proj_plan(plan, rk, nocc_v, nb));
+    key = k2;
+  }
+  PWB_TRY(meta.ensure(2 * sizeof(int)));
+  int hm[2] = {0, nocc};
+  PWB_CUDA(cudaMemcpy(meta.ptr, hm, 2 * sizeof(int), cudaMemcpyHostToDevice));
+  PWB_TRY(part.ensure((size_t)plan.nsplit * ncol * nocc * sizeof(double2)));
+  PWB_TRY(cmat.ensure((size_t)ncol * nocc * sizeof(double2)));
+  ProjArgs a;
+  a.phi = reinterpret_cast<const double2*>(phi);
+  a.off = as<int>(meta);
+  a.nocc = as<int>(meta) + 1;
+  a.tiles = nullptr;
+  a.nbp = nb;
+  a.ldc = nocc;
+  a.nrows_total = ncol;
+  double2* X = reinterpret_cast<double2*>(x);
+  PWB_TRY(proj_coeffs(plan, a, X, as<double2>(part), as<double2>(cmat), nullptr));
+  PWB_TRY(proj_apply(plan, a, as<double2>(cmat), X, X, 1.0, -1.0, nullptr, ncol, nullptr));
+  PWB_CUDA(cudaStreamSynchronize(nullptr));
+  return PWB_OK;
+}
+
+// Pieces of chi0 for a perturbation dv (all bands): diag_host[2*b + {0,1}] =
+// <phi_b, dv phi_b> (complex, response.py:53-55) and, if dphi is non-NULL,
+// the occupied-subspace response Phi (W o M) as device rows (response.py:101-107).
+int pwb_chi0_parts(pwb_state* st, const double* dv, double* diag_host, double* dphi) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  PWB_TRY(st->fsum.ensure(2 * sizeof(double)));
+  PWB_TRY(pwb_chi0_begin(st, 0, st->nband, dv, as<double>(st->fsum)));
+  pwb_grid* g = st->g;
+  cudaStream_t s = g->stream;
+  const int n = st->nband;
+  std::vector<double2> cm((size_t)n * st->ldc);
+  PWB_CUDA(cudaMemcpyAsync(cm.data(), st->cm.ptr, cm.size() * sizeof(double2),
+                           cudaMemcpyDeviceToHost, s));
+  PWB_CUDA(cudaStreamSynchronize(s));
+  for (int b = 0; b < n; ++b) {
+    const int m = b - st->off[st->band_k[b]];
+    diag_host[2 * b] = cm[(size_t)b * st->ldc + m].x;
+    diag_host[2 * b + 1] = cm[(size_t)b * st->ldc + m].y;
+  }
+  if (dphi) {
+    double* deps = as<double>(st->scal);
+    k_chi0_occ<<<n, 64, 0, s>>>(0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_nocc),
+                                as<double>(st->d_coef), as<double>(st->fsum), st->fp_den,
+                                st->fp_thresh, deps, as<double>(st->wt), as<double2>(st->cm),
+                                as<double2>(st->cw), deps + n, deps + 2 * n);
+    PWB_LAUNCH_CHECK();
+    ProjArgs a = proj_args(st);
+    PWB_TRY(proj_apply(st->cg.plan1, a, as<double2>(st->cw), nullptr,
+                       reinterpret_cast<double2*>(dphi), 0.0, 1.0, nullptr, n, s));
+    PWB_CUDA(cudaStreamSynchronize(s));
+  }
+  return PWB_OK;
+}
+
+// orbital_row_norm (response.py:190-199) for arbitrary device sphere rows.
+int pwb_row_norm_rows(pwb_grid* g, int nrows, const int* band_k, const double* rows,
+                      int real_part, double* out_host) {
+  if (!g) return fail(PWB_ERR_VALUE, "null grid");
+  DevBuf cache, res;
+  PWB_TRY(cache.ensure((size_t)std::max(nrows, 1) * g->ng * sizeof(double2)));
+  PWB_TRY(res.ensure(sizeof(double)));
+  PWB_TRY(pwb_to_real(g, nrows, band_k, rows, as<double>(cache)));
+  PWB_TRY(launch_row_norm(g, nrows, as<double2>(cache), real_part, as<double>(res)));
+  double v = 0.0;
+  PWB_CUDA(cudaMemcpyAsync(&v, res.ptr, sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+  PWB_CUDA(cudaStreamSynchronize(g->stream));
+  *out_host = std::sqrt(v);
+  return PWB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// Dense real-vector kernels for the device-resident inexact GMRES
+// (reference igmres.py:86-114).  Dots use a fixed two-stage reduction
+// (fixed grid, fixed order), so every scalar is bitwise reproducible; the
+// MGS step keeps the Hessenberg entries on the device and returns the
+// column to the host once per Arnoldi step.
+#include <cmath>
+
+#include "grid.cuh"
+
+namespace pwb {
+
+constexpr int NTV = 256;
+constexpr int kDotBlocks = 148;
+
+__global__ void __launch_bounds__(NTV) k_dot_partial(int n, const double* __restrict__ x,
+                                                     const double* __restrict__ y,
+                                                     double* __restrict__ part) {
+  __shared__ double red[NTV];
+  double s = 0.0;
+  for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV) s += x[i] * y[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = NTV / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// out[0] = sum(part) (+= when accumulate), optional sqrt
+__global__ void k_dot_final(int np, const double* __restrict__ part, double* __restrict__ out,
+                            int accumulate, int take_sqrt) {
+  __shared__ double red[NTV];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += NTV) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = NTV / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double v = red[0];
+    if (take_sqrt) v = sqrt(v);
+    out[0] = accumulate ? out[0] + v : v;
+  }
+}
+
+// y -= c[0] * x   (c on device; sign flips via neg)
+__global__ void k_axpy_dev(int n, const double* __restrict__ c, const double* __restrict__ x,
+                           double* __restrict__ y) {
+  const double a = c[0];
+  for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV) y[i] -= a * x[i];
+}
+
+__global__ void k_axpy_host(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV) y[i] += a * x[i];
+}
+
+// v = w / h (or 0 when h == 0: lucky breakdown, igmres.py:99-102)
+__global__ void k_normalise(int n, const double* __restrict__ h, const double* __restrict__ w,
+                            double* __restrict__ v) {
+  const double d = h[0];
+  for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV)
+    v[i] = d > 0.0 ? w[i] / d : 0.0;
+}
+
+// x = x0 + sum_j y_j V_j with the reference's sequential order
+__global__ void k_combine(int n, int m, const double* __restrict__ V, const double* __restrict__ y,
+                          const double* __restrict__ x0, double* __restrict__ x) {
+  for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV) {
+    double s = x0[i];
+    for (int j = 0; j < m; ++j) s = s + y[j] * V[(size_t)j * n + i];
+    x[i] = s;
+  }
+}
+
+static int blocks_for(int n) { return std::max(1, std::min(kDotBlocks, (n + NTV - 1) / NTV)); }
+
+static int dot_into(pwb_grid* g, int n, const double* x, const double* y, double* out,
+                    int accumulate, int take_sqrt) {
+  PWB_TRY(g->red.ensure(kDotBlocks * sizeof(double)));
+  const int nb = blocks_for(n);
+  k_dot_partial<<<nb, NTV, 0, g->stream>>>(n, x, y, as<double>(g->red));
+  PWB_LAUNCH_CHECK();
+  k_dot_final<<<1, NTV, 0, g->stream>>>(nb, as<double>(g->red), out, accumulate, take_sqrt);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+}  // namespace pwb
+
+using namespace pwb;
+
+extern "C" {
+
+int pwb_vec_dot(pwb_grid* g, int n, const double* x, const double* y, double* out_dev) {
+  if (!g) return fail(PWB_ERR_VALUE, "null grid");
+  return dot_into(g, n, x, y, out_dev, 0, 0);
+}
+
+int pwb_vec_axpy(pwb_grid* g, int n, double a, const double* x, double* y) {
+  if (!g) return fail(PWB_ERR_VALUE, "null grid");
+  k_axpy_host<<<blocks_for(n), NTV, 0, g->stream>>>(n, a, x, y);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int pwb_arnoldi_mgs(pwb_grid* g, int n, int i, double* basis, double* w, double* hcol_host) {
+  if (!g) return fail(PWB_ERR_VALUE, "null grid");
+  if (i < 0) return fail(PWB_ERR_VALUE, "negative Arnoldi index");
+  PWB_TRY(g->scratch.ensure((size_t)(2 * (i + 1) + 1) * sizeof(double)));
+  double* hd = as<double>(g->scratch);   // [0..i]: pass 1, [i+1..2i+1]: pass 2, [2i+2]: norm
+  const int nb = blocks_for(n);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int j = 0; j <= i; ++j) {
+      double* c = hd + pass * (i + 1) + j;
+      PWB_TRY(dot_into(g, n, basis + (size_t)j * n, w, c, 0, 0));
+      k_axpy_dev<<<nb, NTV, 0, g->stream>>>(n, c, basis + (size_t)j * n, w);
+      PWB_LAUNCH_CHECK();
+    }
+  double* nrm = hd + 2 * (i + 1);
+  PWB_TRY(dot_into(g, n, w, w, nrm, 0, 1));
+  k_normalise<<<nb, NTV, 0, g->stream>>>(n, nrm, w, basis + (size_t)(i + 1) * n);
+  PWB_LAUNCH_CHECK();
+  std::vector<double> hh(2 * (i + 1) + 1);
+  PWB_CUDA(cudaMemcpyAsync(hh.data(), hd, hh.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           g->stream));
+  PWB_CUDA(cudaStreamSynchronize(g->stream));
+  for (int j = 0; j <= i; ++j) hcol_host[j] = hh[j] + hh[i + 1 + j];
+  hcol_host[i + 1] = hh[2 * (i + 1)];
+  return PWB_OK;
+}
+
+int pwb_vec_combine(pwb_grid* g, int n, int m, const double* basis, const double* y_host,
+                    const double* x0, double* x) {
+  if (!g) return fail(PWB_ERR_VALUE, "null grid");
+  PWB_TRY(g->scratch.ensure((size_t)std::max(m, 1) * sizeof(double)));
+  if (m > 0)
+    PWB_CUDA(cudaMemcpyAsync(g->scratch.ptr, y_host, m * sizeof(double), cudaMemcpyHostToDevice,
+                             g->stream));
+  k_combine<<<blocks_for(n), NTV, 0, g->stream>>>(n, m, basis, as<double>(g->scratch), x0, x);
+  PWB_LAUNCH_CHECK();
+  PWB_CUDA(cudaStreamSynchronize(g->stream));
+  return PWB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,256 @@
+"""Device-resident grids and ground states (handles onto libpwb200 objects).
+
+`DeviceGrid` wraps a `pwb_grid` (sphere/cube tables + FFT plans for one or
+more k-points sharing a cube); `DeviceState` wraps a `pwb_state` (occupied
+orbitals, eigenvalues, occupations, V_local and rho in HBM).  Both are built
+once and cached on the host objects they mirror (attribute
+`_pwb_device_grid` / `_pwb_device_state`), the way the reference caches
+row norms on its GroundState (groundstate.py:299).
+
+PyTorch is used only to own device buffers and for torch.distributed
+(NCCL) when the (k, n) batch is sharded over ranks.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import DeviceError
+
+
+def torch_mod():
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the B200 path has no CPU fallback")
+    return torch
+
+
+def ptr(t):
+    """Device pointer of a torch tensor (or None)."""
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _np_ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class DeviceGrid:
+    """pwb_grid for a list of FourierGrids sharing one cube (one per k-point)."""
+
+    def __init__(self, grids_list):
+        torch = torch_mod()
+        lib = _lib.load()
+        _lib.require_device()
+        grids_list = list(grids_list)
+        g0 = grids_list[0]
+        for g in grids_list[1:]:
+            if tuple(g.cube_dims) != tuple(g0.cube_dims):
+                raise ValueError("k-point grids must share one FFT cube")
+        self.grids = grids_list
+        self.cube_dims = tuple(int(d) for d in g0.cube_dims)
+        self.n_g = int(np.prod(self.cube_dims))
+        self.volume = float(g0.lattice.volume)
+        self.nk = len(grids_list)
+        self.nb = [int(g.n_b) for g in grids_list]
+        nb = np.array(self.nb, dtype=np.int32)
+        gint = np.ascontiguousarray(np.concatenate([g.g_int for g in grids_list]).astype(np.int32))
+        g2s = np.ascontiguousarray(np.concatenate([g.g2_sphere for g in grids_list]), dtype=float)
+        g2c = np.ascontiguousarray(g0.g2_cube, dtype=float)
+        handle = ctypes.c_void_p()
+        nx, ny, nz = self.cube_dims
+        _lib.check(lib.pwb_grid_create(nx, ny, nz, self.volume, self.nk, _np_ptr(nb),
+                                       _np_ptr(gint), _np_ptr(g2s), _np_ptr(g2c),
+                                       ctypes.byref(handle)), "pwb_grid_create")
+        self.handle = handle
+        self._lib = lib
+        _lib.check(lib.pwb_grid_set_stream(handle, ctypes.c_void_p(
+            torch.cuda.current_stream().cuda_stream)))
+        info = np.zeros(8, dtype=np.int32)
+        _lib.check(lib.pwb_grid_info(handle, _np_ptr(info)))
+        self.nbp = int(info[4])
+        self.nxa = int(info[5])
+        self.nya = int(info[6])
+        self.tile = int(info[7])
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.pwb_grid_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    # -- packing of sphere rows -------------------------------------------------
+    def rows(self, n):
+        torch = torch_mod()
+        return torch.zeros((n, self.nbp), dtype=torch.complex128, device=self.device)
+
+    def pack(self, vectors, ks=None):
+        """Host sphere vectors (list / 2-D array, row b for k ks[b]) -> padded device rows."""
+        torch = torch_mod()
+        vecs = list(vectors)
+        n = len(vecs)
+        host = np.zeros((n, self.nbp), dtype=np.complex128)
+        for i, v in enumerate(vecs):
+            k = 0 if ks is None else int(ks[i])
+            v = np.asarray(v)
+            if v.shape != (self.nb[k],):
+                raise ValueError(f"expected sphere vector of length {self.nb[k]}, got {v.shape}")
+            host[i, : self.nb[k]] = v
+        return torch.from_numpy(host).to(self.device)
+
+    def unpack(self, rows, ks=None):
+        """Device rows -> list of host sphere vectors (trimmed to n_b of each k)."""
+        host = rows.cpu().numpy()
+        out = []
+        for i in range(host.shape[0]):
+            k = 0 if ks is None else int(ks[i])
+            out.append(host[i, : self.nb[k]].copy())
+        return out
+
+    def band_k_tensor(self, ks):
+        torch = torch_mod()
+        return torch.tensor(np.asarray(ks, dtype=np.int32), dtype=torch.int32, device=self.device)
+
+
+def device_grid(grids_list):
+    """Cached DeviceGrid for one FourierGrids (Gamma) or a tuple of k-grids."""
+    if not isinstance(grids_list, (list, tuple)):
+        grids_list = [grids_list]
+    owner = grids_list[0]
+    key = tuple(id(g) for g in grids_list)
+    cache = getattr(owner, "_pwb_device_grid", None)
+    if cache is not None and cache[0] == key:
+        return cache[1]
+    dg = DeviceGrid(grids_list)
+    try:
+        owner._pwb_device_grid = (key, dg)
+    except AttributeError:
+        pass
+    return dg
+
+
+def state_blocks(gs):
+    """(blocks, weights): the k blocks of a ground state (Gamma -> one block, w=1)."""
+    if hasattr(gs, "blocks"):
+        return list(gs.blocks), np.asarray(gs.weights, dtype=float)
+    return [gs], np.ones(1)
+
+
+class DeviceState:
+    """pwb_state for a (possibly k-sampled) ground state."""
+
+    def __init__(self, gs):
+        torch = torch_mod()
+        lib = _lib.load()
+        blocks, weights = state_blocks(gs)
+        self.gs = gs
+        self.blocks = blocks
+        self.weights = weights
+        self.grid = device_grid([b.grids for b in blocks])
+        self.nocc = [int(b.n_occ) for b in blocks]
+        self.nband = int(sum(self.nocc))
+        self.band_k = np.repeat(np.arange(len(blocks)), self.nocc).astype(np.int32)
+        self.offsets = np.concatenate([[0], np.cumsum(self.nocc)]).astype(int)
+        phi = np.ascontiguousarray(np.concatenate(
+            [np.ascontiguousarray(b.phi_occ.T).ravel() for b in blocks]), dtype=np.complex128)
+        eps = np.ascontiguousarray(np.concatenate([b.eps_occ for b in blocks]), dtype=float)
+        occ = np.ascontiguousarray(np.concatenate([b.occ_occ for b in blocks]), dtype=float)
+        fpr = np.ascontiguousarray(np.concatenate([b.fprime_occ() for b in blocks]), dtype=float)
+        self.eps, self.occ, self.fprime = eps, occ, fpr
+        wb = weights[self.band_k]
+        self.fp_den = float(np.sum(wb * fpr))          # sum_k w_k sum_n f'_nk
+        self.fp_thresh = 1e-14 * float(np.sum(wb))     # response.py:135 with k weights
+        nocc = np.array(self.nocc, dtype=np.int32)
+        w = np.ascontiguousarray(weights, dtype=float)
+        vloc = np.ascontiguousarray(gs.v_local, dtype=float)
+        rho = np.ascontiguousarray(gs.rho, dtype=float)
+        handle = ctypes.c_void_p()
+        _lib.check(lib.pwb_state_create(self.grid.handle, _np_ptr(nocc), _np_ptr(w), _np_ptr(phi),
+                                        _np_ptr(eps), _np_ptr(occ), _np_ptr(fpr), _np_ptr(vloc),
+                                        _np_ptr(rho), ctypes.byref(handle)), "pwb_state_create")
+        self.handle = handle
+        self._lib = lib
+        self.device = self.grid.device
+        self.rho_t = torch.from_numpy(rho).to(self.device)
+        self.vloc_t = torch.from_numpy(vloc).to(self.device)
+        self._fsum = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self.shard = (0, self.nband)
+        self.comm = None
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.pwb_state_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    # -- sharding over ranks ---------------------------------------------------------
+    def set_sharding(self, rank, world, group=None):
+        """Own the contiguous band range of `rank` (k blocks stay whole when N_k >= world)."""
+        self.shard = shard_range(self.nocc, rank, world)
+        self.comm = (rank, world, group) if world > 1 else None
+
+    def chi0(self, dv_t, tol):
+        """drho (device tensor) and per-(k, n) iteration counts of the local shard.
+
+        With sharding active the result is already all-reduced over ranks, and
+        the returned iteration counts cover the whole (k, n) list (all-gathered).
+        """
+        torch = torch_mod()
+        tol = np.ascontiguousarray(tol, dtype=float)
+        drho = torch.empty(self.grid.n_g, dtype=torch.float64, device=self.device)
+        b0, b1 = self.shard
+        if self.comm is None and (b0, b1) == (0, self.nband):
+            its = np.zeros(self.nband, dtype=np.int32)
+            status = self._lib.pwb_chi0(self.handle, ptr(dv_t), _np_ptr(tol), ptr(drho),
+                                        _np_ptr(its))
+            _lib.check(status, "chi0")
+            return drho, its
+        import torch.distributed as dist
+        rank, world, group = self.comm if self.comm else (0, 1, None)
+        _lib.check(self._lib.pwb_chi0_begin(self.handle, b0, b1, ptr(dv_t), ptr(self._fsum)),
+                   "chi0_begin")
+        if self.comm is not None and abs(self.fp_den) > self.fp_thresh:
+            dist.all_reduce(self._fsum[:1], group=group)   # global delta eps_F (metals)
+        its_local = np.zeros(max(b1 - b0, 1), dtype=np.int32)
+        tl = np.ascontiguousarray(tol[b0:b1]) if b1 > b0 else np.zeros(1)
+        status = self._lib.pwb_chi0_finish(self.handle, ptr(self._fsum), _np_ptr(tl), ptr(drho),
+                                           _np_ptr(its_local))
+        if self.comm is not None:
+            dist.all_reduce(drho, group=group)
+            cnt = torch.zeros(self.nband, dtype=torch.int64, device=self.device)
+            cnt[b0:b1] = torch.from_numpy(its_local[: b1 - b0].astype(np.int64)).to(self.device)
+            dist.all_reduce(cnt, group=group)
+            its = cnt.cpu().numpy().astype(np.int32)
+        else:
+            its = its_local[: b1 - b0]
+        _lib.check(status, "chi0_finish")
+        return drho, its
+
+
+def shard_range(nocc, rank, world):
+    """Contiguous [b0, b1) of the (k, n) list for `rank`, balanced by band count."""
+    total = int(sum(nocc))
+    if world <= 1:
+        return 0, total
+    bounds = [round(total * r / world) for r in range(world + 1)]
+    return bounds[rank], bounds[rank + 1]
+
+
+def device_state(gs):
+    """Cached DeviceState of a ground state (the reference's or this package's)."""
+    cache = getattr(gs, "_pwb_device_state", None)
+    if cache is not None:
+        return cache
+    ds = DeviceState(gs)
+    try:
+        object.__setattr__(gs, "_pwb_device_state", ds)
+    except (AttributeError, TypeError):
+        pass
+    return ds
