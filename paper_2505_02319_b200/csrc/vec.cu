@@ -75,15 +75,29 @@ __global__ void k_combine(int n, int m, const double* __restrict__ V, const doub
   }
 }
 
+// vector ops may run without a grid (generic GMRES use): default stream and
+// thread-local scratch
+struct VecCtx {
+  cudaStream_t stream;
+  DevBuf* red;
+  DevBuf* scratch;
+};
+
+static VecCtx vctx(pwb_grid* g) {
+  static thread_local DevBuf red, scratch;
+  if (g) return VecCtx{g->stream, &g->red, &g->scratch};
+  return VecCtx{nullptr, &red, &scratch};
+}
+
 static int blocks_for(int n) { return std::max(1, std::min(kDotBlocks, (n + NTV - 1) / NTV)); }
 
-static int dot_into(pwb_grid* g, int n, const double* x, const double* y, double* out,
+static int dot_into(const VecCtx& c, int n, const double* x, const double* y, double* out,
                     int accumulate, int take_sqrt) {
-  PWB_TRY(g->red.ensure(kDotBlocks * sizeof(double)));
+  PWB_TRY(c.red->ensure(kDotBlocks * sizeof(double)));
   const int nb = blocks_for(n);
-  k_dot_partial<<<nb, NTV, 0, g->stream>>>(n, x, y, as<double>(g->red));
+  k_dot_partial<<<nb, NTV, 0, c.stream>>>(n, x, y, as<double>(*c.red));
   PWB_LAUNCH_CHECK();
-  k_dot_final<<<1, NTV, 0, g->stream>>>(nb, as<double>(g->red), out, accumulate, take_sqrt);
+  k_dot_final<<<1, NTV, 0, c.stream>>>(nb, as<double>(*c.red), out, accumulate, take_sqrt);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -95,38 +109,36 @@ using namespace pwb;
 extern "C" {
 
 int pwb_vec_dot(pwb_grid* g, int n, const double* x, const double* y, double* out_dev) {
-  if (!g) return fail(PWB_ERR_VALUE, "null grid");
-  return dot_into(g, n, x, y, out_dev, 0, 0);
+  return dot_into(vctx(g), n, x, y, out_dev, 0, 0);
 }
 
 int pwb_vec_axpy(pwb_grid* g, int n, double a, const double* x, double* y) {
-  if (!g) return fail(PWB_ERR_VALUE, "null grid");
-  k_axpy_host<<<blocks_for(n), NTV, 0, g->stream>>>(n, a, x, y);
+  k_axpy_host<<<blocks_for(n), NTV, 0, vctx(g).stream>>>(n, a, x, y);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
 
 int pwb_arnoldi_mgs(pwb_grid* g, int n, int i, double* basis, double* w, double* hcol_host) {
-  if (!g) return fail(PWB_ERR_VALUE, "null grid");
   if (i < 0) return fail(PWB_ERR_VALUE, "negative Arnoldi index");
-  PWB_TRY(g->scratch.ensure((size_t)(2 * (i + 1) + 1) * sizeof(double)));
-  double* hd = as<double>(g->scratch);   // [0..i]: pass 1, [i+1..2i+1]: pass 2, [2i+2]: norm
+  const VecCtx c = vctx(g);
+  PWB_TRY(c.scratch->ensure((size_t)(2 * (i + 1) + 1) * sizeof(double)));
+  double* hd = as<double>(*c.scratch);   // [0..i]: pass 1, [i+1..2i+1]: pass 2, [2i+2]: norm
   const int nb = blocks_for(n);
   for (int pass = 0; pass < 2; ++pass)
     for (int j = 0; j <= i; ++j) {
       double* c = hd + pass * (i + 1) + j;
-      PWB_TRY(dot_into(g, n, basis + (size_t)j * n, w, c, 0, 0));
-      k_axpy_dev<<<nb, NTV, 0, g->stream>>>(n, c, basis + (size_t)j * n, w);
+      PWB_TRY(dot_into(vctx(g), n, basis + (size_t)j * n, w, c, 0, 0));
+      k_axpy_dev<<<nb, NTV, 0, vctx(g).stream>>>(n, c, basis + (size_t)j * n, w);
       PWB_LAUNCH_CHECK();
     }
   double* nrm = hd + 2 * (i + 1);
-  PWB_TRY(dot_into(g, n, w, w, nrm, 0, 1));
-  k_normalise<<<nb, NTV, 0, g->stream>>>(n, nrm, w, basis + (size_t)(i + 1) * n);
+  PWB_TRY(dot_into(c, n, w, w, nrm, 0, 1));
+  k_normalise<<<nb, NTV, 0, c.stream>>>(n, nrm, w, basis + (size_t)(i + 1) * n);
   PWB_LAUNCH_CHECK();
   std::vector<double> hh(2 * (i + 1) + 1);
   PWB_CUDA(cudaMemcpyAsync(hh.data(), hd, hh.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                           g->stream));
-  PWB_CUDA(cudaStreamSynchronize(g->stream));
+                           c.stream));
+  PWB_CUDA(cudaStreamSynchronize(c.stream));
   for (int j = 0; j <= i; ++j) hcol_host[j] = hh[j] + hh[i + 1 + j];
   hcol_host[i + 1] = hh[2 * (i + 1)];
   return PWB_OK;
@@ -134,14 +146,14 @@ int pwb_arnoldi_mgs(pwb_grid* g, int n, int i, double* basis, double* w, double*
 
 int pwb_vec_combine(pwb_grid* g, int n, int m, const double* basis, const double* y_host,
                     const double* x0, double* x) {
-  if (!g) return fail(PWB_ERR_VALUE, "null grid");
-  PWB_TRY(g->scratch.ensure((size_t)std::max(m, 1) * sizeof(double)));
+  const VecCtx c = vctx(g);
+  PWB_TRY(c.scratch->ensure((size_t)std::max(m, 1) * sizeof(double)));
   if (m > 0)
-    PWB_CUDA(cudaMemcpyAsync(g->scratch.ptr, y_host, m * sizeof(double), cudaMemcpyHostToDevice,
-                             g->stream));
-  k_combine<<<blocks_for(n), NTV, 0, g->stream>>>(n, m, basis, as<double>(g->scratch), x0, x);
+    PWB_CUDA(cudaMemcpyAsync(c.scratch->ptr, y_host, m * sizeof(double), cudaMemcpyHostToDevice,
+                             c.stream));
+  k_combine<<<blocks_for(n), NTV, 0, c.stream>>>(n, m, basis, as<double>(*c.scratch), x0, x);
   PWB_LAUNCH_CHECK();
-  PWB_CUDA(cudaStreamSynchronize(g->stream));
+  PWB_CUDA(cudaStreamSynchronize(c.stream));
   return PWB_OK;
 }
 
