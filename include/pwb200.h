@@ -55,6 +55,13 @@ int pwb_device_count(int* count);
 /* stream used by subsequent calls on this grid/state (cudaStream_t, NULL = legacy) */
 int pwb_grid_set_stream(pwb_grid* grid, void* stream);
 
+/* live kernel timing (CUDA events on the launching stream) per category:
+ * 0 H apply in CG, 1 projector GEMMs, 2 CG reductions/updates, 3 chi0 RHS,
+ * 4 drho accumulation; arrays of 8.  units = rows (bands) processed.        */
+int pwb_profile_enable(int on);
+int pwb_profile_reset(void);
+int pwb_profile_read(double* ms, long long* count, long long* units);
+
 /* ---- grid / FFT plan:  FourierGrids (pwbasis.py:95-224) --------------------
  * nk k-point spheres sharing one (nx,ny,nz) cube.  g_int: concatenation over
  * k of (nb_k, 3) int32 integer coordinates (lexicographically sorted);

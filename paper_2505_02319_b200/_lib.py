@@ -56,6 +56,9 @@ SIGNATURES = {
     "pwb_row_norm_rows": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int, _c_dbl_p]),
     "pwb_chi0_parts": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "pwb_project_generic": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]),
+    "pwb_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "pwb_profile_reset": (ctypes.c_int, []),
+    "pwb_profile_read": (ctypes.c_int, [_vp, _vp, _vp]),
     "pwb_vec_dot": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
     "pwb_vec_axpy": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_double, _vp, _vp]),
     "pwb_arnoldi_mgs": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
@@ -115,6 +118,26 @@ def device_count():
 
 def launch_count():
     return int(load().pwb_launch_count())
+
+
+PROFILE_CATEGORIES = ("ham_apply", "projector", "cg_vector", "chi0_rhs", "drho_accumulate")
+
+
+def profile(on=True):
+    load().pwb_profile_enable(1 if on else 0)
+    load().pwb_profile_reset()
+
+
+def profile_read():
+    """{category: (ms, launches-groups, units)} accumulated since profile()."""
+    import numpy as np
+    ms = np.zeros(8)
+    cnt = np.zeros(8, dtype=np.int64)
+    units = np.zeros(8, dtype=np.int64)
+    load().pwb_profile_read(ctypes.c_void_p(ms.ctypes.data), ctypes.c_void_p(cnt.ctypes.data),
+                            ctypes.c_void_p(units.ctypes.data))
+    return {name: (float(ms[i]), int(cnt[i]), int(units[i]))
+            for i, name in enumerate(PROFILE_CATEGORIES)}
 
 
 def require_device():

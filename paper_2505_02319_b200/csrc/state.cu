@@ -14,6 +14,7 @@
 #include <memory>
 #include <string>
 
+#include "profile.cuh"
 #include "state.cuh"
 
 namespace pwb {
@@ -295,8 +296,10 @@ static int project(pwb_state* st, CgBatch& cg, const ProjPlan& pl, double2* X, c
                    int band_mod) {
   ProjArgs a = proj_args(st);
   cudaStream_t s = st->g->stream;
+  cudaEvent_t e = prof().begin(s);
   PWB_TRY(proj_coeffs(pl, a, X, as<double2>(cg.part), as<double2>(cg.cmat), s));
   PWB_TRY(proj_apply(pl, a, as<double2>(cg.cmat), X, X, 1.0, -1.0, active, band_mod, s));
+  prof().end(PROF_Q, e, s, pl.nrows);
   return PWB_OK;
 }
 
@@ -329,23 +332,32 @@ static int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, 
   bool failed = false;
   for (int it = 0;; ++it) {
     PWB_TRY(project(st, cg, cg.plan1, p, cg.s.active, n));
+    cudaEvent_t eh = prof().begin(s);
     PWB_TRY(launch_plane_inv(g, n, bk, p, 1.0, W));
     PWB_TRY(launch_pencil_vmul(g, n, W, vloc, 1.0 / g->ng));
     PWB_TRY(launch_plane_fwd(g, n, bk, W, 1.0, p, cg.s.eps, ap));
+    prof().end(PROF_H, eh, s, n);
     PWB_TRY(project(st, cg, cg.plan1, ap, cg.s.active, n));
+    cudaEvent_t ec = prof().begin(s);
     k_cg_alpha<<<n, NTC, 0, s>>>(g->dev, cg.s, n, p, ap, xr);
     PWB_LAUNCH_CHECK();
+    prof().end(PROF_CG, ec, s, n);
     PWB_TRY(project(st, cg, cg.plan2, xr, cg.s.active, n));
+    ec = prof().begin(s);
     k_zero_counters<<<1, 1, 0, s>>>(cg.s.counters);
     PWB_LAUNCH_CHECK();
     k_cg_resid<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z);
     PWB_LAUNCH_CHECK();
+    prof().end(PROF_CG, ec, s, n);
     PWB_CUDA(cudaMemcpyAsync(cg.h_counters, cg.s.counters, 2 * sizeof(int),
                              cudaMemcpyDeviceToHost, s));
     PWB_TRY(project(st, cg, cg.plan1, z, cg.s.active, n));
+    ec = prof().begin(s);
     k_cg_beta<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, p);
     PWB_LAUNCH_CHECK();
+    prof().end(PROF_CG, ec, s, n);
     PWB_CUDA(cudaStreamSynchronize(s));
+    prof().flush();
     if (cg.h_counters[1]) failed = true;
     if (cg.h_counters[0] == 0) break;
   }
@@ -572,9 +584,11 @@ int pwb_chi0_begin(pwb_state* st, int b0, int b1, const double* dv, double* fsum
   const double2* phi = as<double2>(st->phi) + (size_t)b0 * g->nbp;
   const int* bk = as<int>(st->d_band_k) + b0;
   double2* dvpsi = as<double2>(st->dvpsi);
+  cudaEvent_t er = prof().begin(s);
   PWB_TRY(launch_plane_inv(g, n, bk, phi, 1.0, W));
   PWB_TRY(launch_pencil_vmul(g, n, W, dv, 1.0 / g->ng));
   PWB_TRY(launch_plane_fwd(g, n, bk, W, 1.0, nullptr, nullptr, dvpsi));
+  prof().end(PROF_RHS, er, s, n);
   // M^T = (Phi^H dvpsi)^T  (response.py:129)
   ProjArgs a = proj_args(st);
   CgBatch& cg = st->cg;
@@ -618,6 +632,7 @@ int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, d
   // drho accumulation (response.py:150-154)
   double2* W = as<double2>(g->wbuf);
   const int* bk = as<int>(st->d_band_k) + b0;
+  cudaEvent_t ea = prof().begin(s);
   PWB_TRY(launch_plane_inv2(g, n, bk, as<double2>(st->dphi), as<double2>(cg.xr), W));
   const int ntile = (g->nyz + g->dev.tile - 1) / g->dev.tile;
   int nchunk = std::max(1, std::min(n, (2 * kSM + ntile - 1) / ntile));
@@ -625,7 +640,9 @@ int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, d
   PWB_TRY(launch_drho_partial(g, n, W, as<double2>(st->psir), c2, c1, nchunk,
                               as<double>(st->drho_part)));
   PWB_TRY(launch_drho_reduce(g, nchunk, as<double>(st->drho_part), drho));
+  prof().end(PROF_ACC, ea, s, n);
   PWB_CUDA(cudaStreamSynchronize(s));
+  prof().flush();
   return PWB_OK;
 }
 
@@ -762,4 +779,34 @@ int pwb_row_norm_rows(pwb_grid* g, int nrows, const int* band_k, const double* r
   return PWB_OK;
 }
 
+}  // extern "C"
+
+namespace pwb {
+Profiler& prof() {
+  static Profiler p;
+  return p;
+}
+}  // namespace pwb
+
+extern "C" {
+int pwb_profile_enable(int on) {
+  pwb::prof().on = on != 0;
+  return PWB_OK;
+}
+int pwb_profile_reset(void) {
+  cudaDeviceSynchronize();
+  pwb::prof().flush();
+  pwb::prof().reset();
+  return PWB_OK;
+}
+int pwb_profile_read(double* ms, long long* count, long long* units) {
+  cudaDeviceSynchronize();
+  pwb::prof().flush();
+  for (int i = 0; i < pwb::PROF_NCAT; ++i) {
+    ms[i] = pwb::prof().ms[i];
+    count[i] = pwb::prof().count[i];
+    units[i] = pwb::prof().units[i];
+  }
+  return PWB_OK;
+}
 }  // extern "C"
