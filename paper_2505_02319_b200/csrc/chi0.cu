@@ -6,6 +6,7 @@
 // accumulation, so dphi(r) never reaches HBM; bands are reduced in a fixed
 // order inside each CTA and chunk partials are summed in a fixed order, so
 // drho is bitwise reproducible (no floating-point atomics).
+#include "dispatch.cuh"
 #include "state.cuh"
 
 namespace pwb {
@@ -13,6 +14,7 @@ namespace pwb {
 constexpr int NTA = 256;
 constexpr int kMaxOwn = 16;   // tile elements per thread (tile*nx <= 3072 + pad)
 
+template <class FX>
 __global__ void __launch_bounds__(NTA) k_drho_partial(GridDev g, int nband, int per_chunk,
                                                       const double2* __restrict__ W,
                                                       const double2* __restrict__ psir,
@@ -38,7 +40,7 @@ __global__ void __launch_bounds__(NTA) k_drho_partial(GridDev g, int nband, int 
       sm[g.xa[p] * Tp + t] = src[(size_t)p * nyz + t0 + t];
     }
     __syncthreads();
-    fft_lines<NTA>(sm, g.px, nt, Tp, 1, nullptr, true);
+    FX::template run<NTA>(g, sm, nt, Tp, 1, nullptr, true);
     const double a2 = c2[b], a1 = c1[b];
     const double2* ps = psir + (size_t)b * g.ng + (size_t)t0 * nx;
 #pragma unroll
@@ -103,8 +105,10 @@ int launch_drho_partial(pwb_grid* g, int nband, const double2* W, const double2*
   const int ntile = (g->nyz + g->dev.tile - 1) / g->dev.tile;
   const int per = (nband + nchunk - 1) / nchunk;
   dim3 grid(ntile, nchunk);
-  k_drho_partial<<<grid, NTA, pencil_smem(g), g->stream>>>(g->dev, nband, per, W, psir, c2, c1,
-                                                           partial);
+  pencil_variant(g, [&](auto fx) {
+    k_drho_partial<decltype(fx)><<<grid, NTA, pencil_smem(g), g->stream>>>(
+        g->dev, nband, per, W, psir, c2, c1, partial);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -126,8 +130,12 @@ int launch_row_norm(pwb_grid* g, int nband, const double2* psir, int real_part, 
 }
 
 int configure_chi0_kernels(const pwb_grid* g) {
-  PWB_CUDA(cudaFuncSetAttribute(k_drho_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)pencil_smem(g)));
+  cudaError_t e = cudaSuccess;
+  pencil_variant(g, [&](auto fx) {
+    e = cudaFuncSetAttribute(k_drho_partial<decltype(fx)>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pencil_smem(g));
+  });
+  PWB_CUDA(e);
   return PWB_OK;
 }
 

@@ -11,7 +11,7 @@
 // eigenvalue-shift epilogue, so H psi costs three passes over the pruned
 // plane buffer ("Kernels").  Only nxa of nx planes (the sphere
 // occupies |ix| <= ~N/4 of the 2x-oversampled cube) are ever stored.
-#include "grid.cuh"
+#include "dispatch.cuh"
 
 namespace pwb {
 
@@ -19,6 +19,7 @@ constexpr int NT = 256;
 
 // ----------------------------------------------------------------------------
 // plane pass, inverse: sphere rows -> W[b][p]
+template <class FY, class FZ>
 __global__ void __launch_bounds__(NT) k_plane_inv(GridDev g, const double2* __restrict__ psi,
                                                   const double2* __restrict__ psi2,
                                                   const int* __restrict__ band_k, double scale,
@@ -41,14 +42,15 @@ __global__ void __launch_bounds__(NT) k_plane_inv(GridDev g, const double2* __re
     for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(src[s], scale);
   }
   __syncthreads();
-  fft_lines<NT>(sm, g.pz, g.nya, g.ny, 0, g.ya, true);   // z lines of active y
-  fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, true);  // y lines, every z
+  FZ::template run<NT>(g, sm, g.nya, g.ny, 0, g.ya, true);   // z lines of active y
+  FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, true);  // y lines, every z
   double2* dst = W + ((size_t)b * g.nxa + p) * nyz;
   for (int i = threadIdx.x; i < nyz; i += NT) dst[i] = sm[i];
 }
 
 // plane pass, forward: W[b][p] -> sphere rows with epilogue
 //   out[s] = a * F(W)[pp[s]] + (kin[s] - shift[b]) * psi_in[s]
+template <class FY, class FZ>
 __global__ void __launch_bounds__(NT) k_plane_fwd(GridDev g, const double2* __restrict__ W,
                                                   const int* __restrict__ band_k, double a,
                                                   const double2* __restrict__ psi_in,
@@ -62,8 +64,8 @@ __global__ void __launch_bounds__(NT) k_plane_fwd(GridDev g, const double2* __re
   const double2* srcw = W + ((size_t)b * g.nxa + p) * nyz;
   for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = srcw[i];
   __syncthreads();
-  fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, false);  // y lines, every z
-  fft_lines<NT>(sm, g.pz, g.nya, g.ny, 0, g.ya, false);    // z lines of active y
+  FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, false);  // y lines, every z
+  FZ::template run<NT>(g, sm, g.nya, g.ny, 0, g.ya, false);    // z lines of active y
   const int s0 = g.xr[k * (g.nxa + 1) + p];
   const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
   const int* pp = g.pp + (size_t)k * g.nbp;
@@ -110,7 +112,7 @@ struct PencilArgs {
   double lda_c;
 };
 
-template <int IN, int OUT>
+template <int IN, int OUT, class FX>
 __global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
   extern __shared__ double2 sm[];
   const int T = g.tile, Tp = g.tilep, nx = g.nx, nyz = g.nyz;
@@ -136,9 +138,9 @@ __global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
   }
   __syncthreads();
   if (a.mode == 1) {
-    fft_lines<NT>(sm, g.px, nt, Tp, 1, nullptr, false);
+    FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, false);
   } else if (a.mode >= 2) {
-    fft_lines<NT>(sm, g.px, nt, Tp, 1, nullptr, true);
+    FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, true);
     if (a.mode == 3) {
       const double* vv = a.v + (size_t)t0 * nx;
       for (int i = threadIdx.x; i < nt * nx; i += NT) {
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
         sm[x * Tp + t] = cscale(sm[x * Tp + t], vv[i] * a.vscale);
       }
       __syncthreads();
-      fft_lines<NT>(sm, g.px, nt, Tp, 1, nullptr, false);
+      FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, false);
     }
   }
   if (OUT == 0) {
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
 //   mode 0: transform (forward: y then z; inverse: z then y)
 //   mode 1: Hartree  D = 4 pi / |G|^2 (0 at G = 0)     fwd -> *D -> inv
 //   mode 2: Kerker   D = |G|^2/(|G|^2+alpha^2) (1 at G=0)
+template <class FY, class FZ>
 __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restrict__ Wf, int mode,
                                                    double param, int inverse) {
   extern __shared__ double2 sm[];
@@ -190,11 +193,11 @@ __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restric
   for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = pl[i];
   __syncthreads();
   if (mode == 0 && inverse) {
-    fft_lines<NT>(sm, g.pz, g.ny, g.ny, 1, nullptr, true);
-    fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, true);
+    FZ::template run<NT>(g, sm, g.ny, g.ny, 1, nullptr, true);
+    FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, true);
   } else {
-    fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, false);
-    fft_lines<NT>(sm, g.pz, g.ny, g.ny, 1, nullptr, false);
+    FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, false);
+    FZ::template run<NT>(g, sm, g.ny, g.ny, 1, nullptr, false);
   }
   if (mode != 0) {
     const double* g2 = g.g2w + (size_t)x * nyz;
@@ -206,13 +209,12 @@ __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restric
       sm[i] = cscale(sm[i], d);
     }
     __syncthreads();
-    fft_lines<NT>(sm, g.pz, g.ny, g.ny, 1, nullptr, true);
-    fft_lines<NT>(sm, g.py, g.nz, 1, g.ny, nullptr, true);
+    FZ::template run<NT>(g, sm, g.ny, g.ny, 1, nullptr, true);
+    FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, true);
   }
   for (int i = threadIdx.x; i < nyz; i += NT) pl[i] = sm[i];
 }
 
-// ----------------------------------------------------------------------------
 size_t plane_smem(const pwb_grid* g) { return (size_t)g->nyz * sizeof(double2); }
 size_t pencil_smem(const pwb_grid* g) { return (size_t)g->nx * g->dev.tilep * sizeof(double2); }
 
@@ -228,7 +230,10 @@ int launch_plane_inv(pwb_grid* g, int nband, const int* band_k, const double2* p
   PWB_TRY(check_band_count(nband));
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
-  k_plane_inv<<<grid, NT, plane_smem(g), g->stream>>>(g->dev, psi, nullptr, band_k, scale, W);
+  plane_variant(g, [&](auto fy, auto fz) {
+    k_plane_inv<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
+        g->dev, psi, nullptr, band_k, scale, W);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -238,7 +243,10 @@ int launch_plane_inv2(pwb_grid* g, int nband, const int* band_k, const double2* 
   PWB_TRY(check_band_count(nband));
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
-  k_plane_inv<<<grid, NT, plane_smem(g), g->stream>>>(g->dev, a, b, band_k, 1.0, W);
+  plane_variant(g, [&](auto fy, auto fz) {
+    k_plane_inv<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
+        g->dev, a, b, band_k, 1.0, W);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -248,7 +256,10 @@ int launch_plane_fwd(pwb_grid* g, int nband, const int* band_k, const double2* W
   PWB_TRY(check_band_count(nband));
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
-  k_plane_fwd<<<grid, NT, plane_smem(g), g->stream>>>(g->dev, W, band_k, a, psi_in, shift, out);
+  plane_variant(g, [&](auto fy, auto fz) {
+    k_plane_fwd<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
+        g->dev, W, band_k, a, psi_in, shift, out);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -277,7 +288,9 @@ int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, doub
   a.nxout = g->nxa;
   a.out_stride = a.in_stride;
   dim3 grid(tiles(g), nband);
-  k_pencil<0, 0><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  pencil_variant(g, [&](auto fx) {
+    k_pencil<0, 0, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -295,7 +308,9 @@ int launch_pencil_to_cube(pwb_grid* g, int nband, const double2* W, double scale
   a.out_stride = (size_t)g->ng;
   a.oscale = scale;
   dim3 grid(tiles(g), nband);
-  k_pencil<0, 1><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  pencil_variant(g, [&](auto fx) {
+    k_pencil<0, 1, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -312,7 +327,9 @@ int launch_pencil_from_cube(pwb_grid* g, int nband, const double2* in, double2* 
   a.nxout = g->nxa;
   a.out_stride = (size_t)g->nxa * g->nyz;
   dim3 grid(tiles(g), nband);
-  k_pencil<1, 0><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  pencil_variant(g, [&](auto fx) {
+    k_pencil<1, 0, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -332,9 +349,13 @@ int launch_full_from_natural(pwb_grid* g, int nvec, const double2* in_c, const d
   a.out_stride = (size_t)g->ng;
   dim3 grid(tiles(g), nvec);
   if (in_c)
-    k_pencil<1, 0><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    pencil_variant(g, [&](auto fx) {
+    k_pencil<1, 0, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  });
   else
-    k_pencil<2, 0><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    pencil_variant(g, [&](auto fx) {
+    k_pencil<2, 0, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -343,7 +364,10 @@ int launch_full_plane(pwb_grid* g, int nvec, double2* Wf, int mode, double param
   PWB_TRY(check_band_count(nvec));
   if (nvec == 0) return PWB_OK;
   dim3 grid(g->nx, nvec);
-  k_plane_full<<<grid, NT, plane_smem(g), g->stream>>>(g->dev, Wf, mode, param, inverse);
+  plane_variant(g, [&](auto fy, auto fz) {
+    k_plane_full<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
+        g->dev, Wf, mode, param, inverse);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -368,9 +392,13 @@ int launch_full_to_natural(pwb_grid* g, int nvec, const double2* Wf, int mode, d
   a.lda_c = -(1.0 / 3.0) * cbrt(3.0 / M_PI);
   dim3 grid(tiles(g), nvec);
   if (out_c)
-    k_pencil<0, 1><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    pencil_variant(g, [&](auto fx) {
+    k_pencil<0, 1, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  });
   else
-    k_pencil<0, 2><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    pencil_variant(g, [&](auto fx) {
+    k_pencil<0, 2, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+  });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -379,14 +407,30 @@ int configure_kernels(const pwb_grid* g) {
   const size_t ps = plane_smem(g), cs = pencil_smem(g);
   if (ps > 227 * 1024 || cs > 227 * 1024)
     return fail(PWB_ERR_UNSUPPORTED, "grid plane does not fit in shared memory");
-  PWB_CUDA(cudaFuncSetAttribute(k_plane_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps));
-  PWB_CUDA(cudaFuncSetAttribute(k_plane_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps));
-  PWB_CUDA(cudaFuncSetAttribute(k_plane_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps));
-  PWB_CUDA(cudaFuncSetAttribute(k_pencil<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
-  PWB_CUDA(cudaFuncSetAttribute(k_pencil<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
-  PWB_CUDA(cudaFuncSetAttribute(k_pencil<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
-  PWB_CUDA(cudaFuncSetAttribute(k_pencil<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
-  PWB_CUDA(cudaFuncSetAttribute(k_pencil<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+  cudaError_t e = cudaSuccess;
+  plane_variant(g, [&](auto fy, auto fz) {
+    using FY = decltype(fy);
+    using FZ = decltype(fz);
+    e = cudaFuncSetAttribute(k_plane_inv<FY, FZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_plane_fwd<FY, FZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_plane_full<FY, FZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
+  });
+  PWB_CUDA(e);
+  pencil_variant(g, [&](auto fx) {
+    using FX = decltype(fx);
+    e = cudaFuncSetAttribute(k_pencil<0, 0, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_pencil<0, 1, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_pencil<0, 2, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_pencil<1, 0, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_pencil<2, 0, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+  });
+  PWB_CUDA(e);
   return PWB_OK;
 }
 

@@ -1,0 +1,231 @@
+// Compile-time specialised line FFTs (lengths used by the BASELINE grids and
+// the reference's test grids).  Same in-place Stockham scheme as
+// fft_engine.cuh, but with N, the radix sequence and every index constant
+// known to the compiler: no runtime divisions, no predicated radix slots,
+// radix-16/6 codelets so 48 = 16x3, 64 = 16x4, 96 = 16x6 take two passes.
+// ncu on the runtime engine showed ~300 instructions per element per line
+// FFT at n = 48; this path is what the kernels use whenever a size has a
+// plan below (fft_kernels.cu dispatch), the runtime engine otherwise.
+#pragma once
+
+#include "grid.cuh"
+
+namespace pwb {
+
+// W_16^q = exp(sgn * 2 pi i q / 16) applied to v
+__device__ __forceinline__ double2 w16(double2 v, int q, double sgn) {
+  const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
+  const double h = 0.70710678118654752440;
+  double c, s;
+  switch (q) {
+    case 0: return v;
+    case 1: c = c1; s = s1; break;
+    case 2: c = h; s = h; break;
+    case 3: c = s1; s = c1; break;
+    case 4: return cmul_isgn(v, sgn);
+    case 6: c = -h; s = h; break;
+    case 9: c = -c1; s = -s1; break;
+    default: c = 1.0; s = 0.0; break;
+  }
+  const double ss = sgn * s;
+  return make_double2(v.x * c - v.y * ss, v.x * ss + v.y * c);
+}
+
+template <>
+struct Dft<16> {
+  static __device__ __forceinline__ void run(double2* v, double sgn) {
+    double2 y[4][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+      double2 a[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
+      Dft<4>::run(a, sgn);
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) y[n2][k1] = w16(a[k1], n2 * k1, sgn);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      double2 b[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
+      Dft<4>::run(b, sgn);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = b[k2];
+    }
+  }
+};
+
+template <>
+struct Dft<6> {
+  // 6 = 2 (inner, n1) x 3 (outer, n2): x[3 n1 + n2], X[k1 + 2 k2]
+  static __device__ __forceinline__ void run(double2* v, double sgn) {
+    const double s3 = 0.86602540378443864676;
+    double2 y0[3], y1[3];
+#pragma unroll
+    for (int n2 = 0; n2 < 3; ++n2) {
+      y0[n2] = cadd(v[n2], v[3 + n2]);
+      y1[n2] = csub(v[n2], v[3 + n2]);
+    }
+    // twiddles W6^(n2*k1) for k1 = 1: n2=1 -> (1/2, sgn s3), n2=2 -> (-1/2, sgn s3)
+    y1[1] = cmul(y1[1], make_double2(0.5, sgn * s3));
+    y1[2] = cmul(y1[2], make_double2(-0.5, sgn * s3));
+    Dft<3>::run(y0, sgn);
+    Dft<3>::run(y1, sgn);
+#pragma unroll
+    for (int k2 = 0; k2 < 3; ++k2) {
+      v[2 * k2] = y0[k2];
+      v[1 + 2 * k2] = y1[k2];
+    }
+  }
+};
+
+// One compile-time Stockham pass (radix R, sub-transform size NS) over whole
+// lines, one butterfly per thread per round.
+template <int N, int R, int NS, int NT>
+__device__ __forceinline__ void spass(double2* __restrict__ s, int nlines, int es, int ls,
+                                      const int* __restrict__ lbase,
+                                      const double2* __restrict__ tw, bool inv, bool line_major) {
+  constexpr int NBF = N / R;
+  constexpr int LPR = (NT / NBF) > 0 ? (NT / NBF) : 1;   // whole lines per round
+  constexpr int TWS = N / (NS * R);
+  const double sgn = inv ? 1.0 : -1.0;
+  const int tid = threadIdx.x;
+  int l_in, j;
+  if (line_major) {
+    l_in = tid / NBF;
+    j = tid - l_in * NBF;
+  } else {
+    j = tid / LPR;
+    l_in = tid - j * LPR;
+  }
+  const bool lane_ok = (l_in < LPR) && (j < NBF);
+  const int k = j % NS;
+  const int o0 = (j - k) * R + k;
+  // twiddles for this thread's butterfly are the same in every round
+  double2 w[R];
+  if (NS > 1 && lane_ok) {
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      double2 t = __ldg(&tw[r * k * TWS]);
+      if (inv) t.y = -t.y;
+      w[r] = t;
+    }
+  }
+#pragma unroll 1
+  for (int l0 = 0; l0 < nlines; l0 += LPR) {
+    const int l = l0 + l_in;
+    const bool ok = lane_ok && (l < nlines);
+    double2 v[R];
+    int base = 0;
+    if (ok) {
+      base = lbase ? lbase[l] : l * ls;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = s[base + (j + r * NBF) * es];
+    }
+    __syncthreads();
+    if (ok) {
+      if (NS > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
+      }
+      Dft<R>::run(v, sgn);
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[base + (o0 + r * NS) * es] = v[r];
+    }
+    __syncthreads();
+  }
+}
+
+template <int N, int NS, int... Rs>
+struct Passes;
+
+template <int N, int NS>
+struct Passes<N, NS> {
+  template <int NT>
+  static __device__ __forceinline__ void run(double2*, int, int, int, const int*, const double2*,
+                                            bool, bool) {}
+};
+
+template <int N, int NS, int R, int... Rest>
+struct Passes<N, NS, R, Rest...> {
+  template <int NT>
+  static __device__ __forceinline__ void run(double2* s, int nl, int es, int ls, const int* lb,
+                                            const double2* tw, bool inv, bool lm) {
+    spass<N, R, NS, NT>(s, nl, es, ls, lb, tw, inv, lm);
+    Passes<N, NS * R, Rest...>::template run<NT>(s, nl, es, ls, lb, tw, inv, lm);
+  }
+};
+
+// radix plans (first pass first)
+template <int N>
+struct StaticPlan {
+  static constexpr bool ok = false;
+};
+#define PWB_PLAN(N, ...)                                                                  \
+  template <>                                                                            \
+  struct StaticPlan<N> {                                                                 \
+    static constexpr bool ok = true;                                                     \
+    template <int NT>                                                                    \
+    static __device__ __forceinline__ void run(double2* s, int nl, int es, int ls,       \
+                                              const int* lb, const double2* tw, bool inv) { \
+      Passes<N, 1, __VA_ARGS__>::template run<NT>(s, nl, es, ls, lb, tw, inv, es == 1);  \
+    }                                                                                    \
+  };
+PWB_PLAN(6, 6)
+PWB_PLAN(8, 8)
+PWB_PLAN(12, 4, 3)
+PWB_PLAN(16, 16)
+PWB_PLAN(24, 8, 3)
+PWB_PLAN(32, 8, 4)
+PWB_PLAN(48, 16, 3)
+PWB_PLAN(64, 16, 4)
+PWB_PLAN(96, 16, 6)
+PWB_PLAN(216, 6, 6, 6)
+PWB_PLAN(320, 16, 4, 5)
+#undef PWB_PLAN
+
+// line-FFT policies used to template the transform kernels
+struct DynX {
+  template <int NT>
+  static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
+                                            int ls, const int* lb, bool inv) {
+    fft_lines<NT>(s, g.px, nl, es, ls, lb, inv);
+  }
+};
+struct DynY {
+  template <int NT>
+  static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
+                                            int ls, const int* lb, bool inv) {
+    fft_lines<NT>(s, g.py, nl, es, ls, lb, inv);
+  }
+};
+struct DynZ {
+  template <int NT>
+  static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
+                                            int ls, const int* lb, bool inv) {
+    fft_lines<NT>(s, g.pz, nl, es, ls, lb, inv);
+  }
+};
+template <int N>
+struct StX {
+  template <int NT>
+  static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
+                                            int ls, const int* lb, bool inv) {
+    StaticPlan<N>::template run<NT>(s, nl, es, ls, lb, g.px.tw, inv);
+  }
+};
+template <int N>
+struct StY {
+  template <int NT>
+  static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
+                                            int ls, const int* lb, bool inv) {
+    StaticPlan<N>::template run<NT>(s, nl, es, ls, lb, g.py.tw, inv);
+  }
+};
+template <int N>
+struct StZ {
+  template <int NT>
+  static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
+                                            int ls, const int* lb, bool inv) {
+    StaticPlan<N>::template run<NT>(s, nl, es, ls, lb, g.pz.tw, inv);
+  }
+};
+
+}  // namespace pwb
