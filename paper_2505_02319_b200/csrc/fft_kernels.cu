@@ -23,20 +23,22 @@ template <class FY, class FZ>
 __global__ void __launch_bounds__(NT) k_plane_inv(GridDev g, const double2* __restrict__ psi,
                                                   const double2* __restrict__ psi2,
                                                   const int* __restrict__ band_k, double scale,
-                                                  double2* __restrict__ W) {
+                                                  double2* __restrict__ W,
+                                                  const int* __restrict__ rows) {
   extern __shared__ double2 sm[];
   const int p = blockIdx.x;
-  const int b = blockIdx.y;
-  const int k = band_k ? band_k[b] : 0;
+  const int b = blockIdx.y;                     // plane-buffer slot
+  const int row = rows ? rows[b] : b;           // sphere row (active-row compaction)
+  const int k = band_k ? band_k[row] : 0;
   const int nyz = g.nyz;
   for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = make_double2(0.0, 0.0);
   __syncthreads();
   const int s0 = g.xr[k * (g.nxa + 1) + p];
   const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
-  const double2* src = psi + (size_t)b * g.nbp;
+  const double2* src = psi + (size_t)row * g.nbp;
   const int* pp = g.pp + (size_t)k * g.nbp;
   if (psi2) {
-    const double2* src2 = psi2 + (size_t)b * g.nbp;
+    const double2* src2 = psi2 + (size_t)row * g.nbp;
     for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(cadd(src[s], src2[s]), scale);
   } else {
     for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(src[s], scale);
@@ -55,13 +57,15 @@ __global__ void __launch_bounds__(NT) k_plane_fwd(GridDev g, const double2* __re
                                                   const int* __restrict__ band_k, double a,
                                                   const double2* __restrict__ psi_in,
                                                   const double* __restrict__ shift,
-                                                  double2* __restrict__ out) {
+                                                  double2* __restrict__ out,
+                                                  const int* __restrict__ rows) {
   extern __shared__ double2 sm[];
   const int p = blockIdx.x;
-  const int b = blockIdx.y;
+  const int slot = blockIdx.y;                  // plane-buffer slot
+  const int b = rows ? rows[slot] : slot;       // sphere row
   const int k = band_k ? band_k[b] : 0;
   const int nyz = g.nyz;
-  const double2* srcw = W + ((size_t)b * g.nxa + p) * nyz;
+  const double2* srcw = W + ((size_t)slot * g.nxa + p) * nyz;
   for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = srcw[i];
   __syncthreads();
   FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, false);  // y lines, every z
@@ -226,13 +230,13 @@ static int check_band_count(int n) {
 }
 
 int launch_plane_inv(pwb_grid* g, int nband, const int* band_k, const double2* psi, double scale,
-                     double2* W) {
+                     double2* W, const int* rows) {
   PWB_TRY(check_band_count(nband));
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
     k_plane_inv<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
-        g->dev, psi, nullptr, band_k, scale, W);
+        g->dev, psi, nullptr, band_k, scale, W, rows);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -245,20 +249,20 @@ int launch_plane_inv2(pwb_grid* g, int nband, const int* band_k, const double2* 
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
     k_plane_inv<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
-        g->dev, a, b, band_k, 1.0, W);
+        g->dev, a, b, band_k, 1.0, W, nullptr);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
 
 int launch_plane_fwd(pwb_grid* g, int nband, const int* band_k, const double2* W, double a,
-                     const double2* psi_in, const double* shift, double2* out) {
+                     const double2* psi_in, const double* shift, double2* out, const int* rows) {
   PWB_TRY(check_band_count(nband));
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
     k_plane_fwd<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
-        g->dev, W, band_k, a, psi_in, shift, out);
+        g->dev, W, band_k, a, psi_in, shift, out, rows);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;

@@ -1,164 +1,210 @@
-// Occupied-subspace projector Q = 1 - Phi Phi^H as two complex-FP64 GEMMs
-// (reference: sternheimer.py:28-30, response.py:129,138).
+// Occupied-subspace projector Q = 1 - Phi Phi^H as two complex-FP64 GEMMs on
+// the FP64 tensor pipe (DMMA: mma.sync.m8n8k4.f64), reference
+// sternheimer.py:28-30 and response.py:129,138.
 //
-//   partial:  C_s[row][m] = sum_{g in split s} conj(Phi_k[m][g]) X[row][g]
-//   reduce :  C[row][m]   = sum_s C_s[row][m]          (fixed split order)
-//   apply  :  Y[row][g]   = a X[row][g] + b sum_m Phi_k[m][g] C[row][m]
+//   coef :  C[row][m] = sum_g conj(Phi_k[m][g]) X[row][g]
+//           split-K over the sphere (grid covers the 148 SMs); warps of a CTA
+//           reduce in smem, CTAs reduce through a partial buffer in FIXED
+//           split order by the last CTA to finish (threadfence + counter):
+//           bitwise reproducible, one launch.
+//   apply:  Y[row][g] = a X[row][g] + b sum_m Phi_k[m][g] C[row][m]
 //
-// Rows of X are grouped in tiles of <= 32 consecutive rows sharing one
-// k block.  The contraction dimension (the padded sphere, up to ~16k for
-// config 4) is split so the grid covers the 148 SMs; the split partials are
-// reduced in a fixed order, so results are bitwise reproducible.
+// Complex products are four real DMMAs (re.re, im.im, re.im, im.re).  Rows of
+// X are grouped in tiles of <= 16 rows sharing one k block; with active-row
+// compaction the tile rows index X through a row list.
+// Measured on B200: DMMA 37.1 TFLOP/s, DFMA 34.0 TFLOP/s (tools/fp64_peak.cu).
 #include "proj.cuh"
 
 namespace pwb {
 
-constexpr int TR = 32;      // rows per tile
-constexpr int TM = 32;      // m per tile (partial)
-constexpr int TS = 32;      // g sub-chunk (partial)
-constexpr int AS = 64;      // g chunk (apply)
+constexpr int TR = 16;   // rows per tile (2 DMMA n-fragments)
+constexpr int CM = 32;   // m per coef block (4 DMMA m-fragments)
+constexpr int CW = 4;    // warps per CTA
+constexpr int AG = 128;  // g per apply CTA (4 warps x 32)
 
-// 64 threads, 4x4 (rows x m) per thread.
-__global__ void __launch_bounds__(64) k_proj_partial(ProjArgs a, const double2* __restrict__ X,
-                                                     int split_len, double2* __restrict__ part) {
-  __shared__ double2 xs[TR][TS + 1];
-  __shared__ double2 ps[TM][TS + 1];
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ int xrow(const ProjArgs& a, const ProjTile& t, int r) {
+  return a.rows ? a.rows[t.row0 + r] : t.row0 + r;
+}
+
+// grid (tiles, m blocks, splits), 128 threads
+__global__ void __launch_bounds__(CW * 32) k_proj_coef(ProjArgs a, const double2* __restrict__ X,
+                                                       int split_len, int nsplit,
+                                                       double2* __restrict__ part,
+                                                       double2* __restrict__ C,
+                                                       unsigned* __restrict__ counters) {
+  __shared__ double2 red[CW][CM][TR];
+  __shared__ bool last;
   const ProjTile t = a.tiles[blockIdx.x];
-  const int m0 = blockIdx.y * TM;
+  const int m0 = blockIdx.y * CM;
   const int nocc = a.nocc[t.k];
   if (m0 >= nocc) return;
   const int split = blockIdx.z;
   const int g0 = split * split_len;
   const int g1 = min(a.nbp, g0 + split_len);
   const double2* phi = a.phi + (size_t)a.off[t.k] * a.nbp;
-  const int tr = threadIdx.x & 7, tm = threadIdx.x >> 3;
-  double2 acc[4][4];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r4 = lane >> 2, c4 = lane & 3;
+  // fragment source rows
+  const double2* prow[4];
+  bool pok[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int ma = 0; ma < 4; ++ma) {
+    const int m = m0 + 8 * ma + r4;
+    pok[ma] = m < nocc;
+    prow[ma] = phi + (size_t)(pok[ma] ? m : 0) * a.nbp;
+  }
+  const double2* xrw[2];
+  bool xok[2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
-
-  for (int gs = g0; gs < g1; gs += TS) {
-    const int len = min(TS, g1 - gs);
-    for (int e = threadIdx.x; e < TR * TS; e += 64) {
-      const int r = e / TS, c = e - r * TS;
-      double2 xv = make_double2(0.0, 0.0), pv = make_double2(0.0, 0.0);
-      if (c < len) {
-        if (r < t.nrows) xv = X[(size_t)(t.row0 + r) * a.nbp + gs + c];
-        if (m0 + r < nocc) pv = phi[(size_t)(m0 + r) * a.nbp + gs + c];
+  for (int nb = 0; nb < 2; ++nb) {
+    const int r = 8 * nb + r4;
+    xok[nb] = r < t.nrows;
+    xrw[nb] = X + (size_t)(xok[nb] ? xrow(a, t, r) : 0) * a.nbp;
+  }
+  double cr[4][2][2], ci[4][2][2];
+#pragma unroll
+  for (int ma = 0; ma < 4; ++ma)
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      cr[ma][nb][0] = cr[ma][nb][1] = 0.0;
+      ci[ma][nb][0] = ci[ma][nb][1] = 0.0;
+    }
+  for (int g = g0 + 4 * w; g < g1; g += 4 * CW) {
+    const int gg = g + c4;
+    const bool gok = gg < g1;
+    double2 av[4], bv[2];
+#pragma unroll
+    for (int ma = 0; ma < 4; ++ma)
+      av[ma] = (gok && pok[ma]) ? __ldg(&prow[ma][gg]) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+      bv[nb] = (gok && xok[nb]) ? xrw[nb][gg] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int ma = 0; ma < 4; ++ma)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        // conj(phi) * x : re = pr xr + pi xi ; im = pr xi - pi xr
+        dmma(cr[ma][nb][0], cr[ma][nb][1], av[ma].x, bv[nb].x);
+        dmma(cr[ma][nb][0], cr[ma][nb][1], av[ma].y, bv[nb].y);
+        dmma(ci[ma][nb][0], ci[ma][nb][1], av[ma].x, bv[nb].y);
+        dmma(ci[ma][nb][0], ci[ma][nb][1], -av[ma].y, bv[nb].x);
       }
-      xs[r][c] = xv;
-      ps[r][c] = pv;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int c = 0; c < TS; ++c) {
-      double2 xv[4], pv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) xv[i] = xs[tr + 8 * i][c];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) pv[j] = ps[tm + 8 * j][c];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          // conj(p) * x
-          acc[i][j].x = fma(pv[j].x, xv[i].x, acc[i][j].x);
-          acc[i][j].x = fma(pv[j].y, xv[i].y, acc[i][j].x);
-          acc[i][j].y = fma(pv[j].x, xv[i].y, acc[i][j].y);
-          acc[i][j].y = fma(-pv[j].y, xv[i].x, acc[i][j].y);
-        }
-    }
-    __syncthreads();
   }
-  double2* out = part + (size_t)split * a.nrows_total * a.ldc;
+  // D fragment: (m = r4, row = 2 c4 + {0,1}) of each (ma, nb) tile
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = tr + 8 * i;
-    if (r >= t.nrows) continue;
+  for (int ma = 0; ma < 4; ++ma)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int m = m0 + tm + 8 * j;
-      if (m < nocc) out[(size_t)(t.row0 + r) * a.ldc + m] = acc[i][j];
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        red[w][8 * ma + r4][8 * nb + 2 * c4 + h] = make_double2(cr[ma][nb][h], ci[ma][nb][h]);
+  __syncthreads();
+  // fixed-order sum over warps -> this split's partial
+  const size_t tile_id = (size_t)blockIdx.x * gridDim.y + blockIdx.y;
+  double2* mypart = part + ((size_t)split * gridDim.x * gridDim.y + tile_id) * (CM * TR);
+  for (int i = threadIdx.x; i < CM * TR; i += CW * 32) {
+    const int m = i / TR, r = i - m * TR;
+    double2 s = red[0][m][r];
+#pragma unroll
+    for (int q = 1; q < CW; ++q) s = cadd(s, red[q][m][r]);
+    if (nsplit == 1) {
+      if (r < t.nrows && m0 + m < nocc) C[(size_t)(t.row0 + r) * a.ldc + m0 + m] = s;
+    } else {
+      mypart[i] = s;
     }
   }
+  if (nsplit == 1) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&counters[tile_id], 1u);
+    last = (prev == (unsigned)nsplit - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const size_t stride = (size_t)gridDim.x * gridDim.y * (CM * TR);
+  const double2* p0 = part + tile_id * (CM * TR);
+  for (int i = threadIdx.x; i < CM * TR; i += CW * 32) {
+    const int m = i / TR, r = i - m * TR;
+    double2 s = p0[i];
+    for (int q = 1; q < nsplit; ++q) s = cadd(s, p0[(size_t)q * stride + i]);
+    if (r < t.nrows && m0 + m < nocc) C[(size_t)(t.row0 + r) * a.ldc + m0 + m] = s;
+  }
+  if (threadIdx.x == 0) counters[tile_id] = 0u;
 }
 
-// C[row][m] = sum_s part[s][row][m], fixed order.
-__global__ void k_proj_reduce(int nsplit, size_t n, const double2* __restrict__ part,
-                              double2* __restrict__ C) {
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double2 s = part[i];
-  for (int q = 1; q < nsplit; ++q) s = cadd(s, part[(size_t)q * n + i]);
-  C[i] = s;
-}
-
-// 128 threads, tile 32 rows x 64 g, 4x4 (rows x g) per thread.
-__global__ void __launch_bounds__(128) k_proj_apply(ProjArgs a, const double2* __restrict__ C,
-                                                    const double2* __restrict__ Xin,
-                                                    double2* __restrict__ Y, double ca, double cb,
-                                                    const int* __restrict__ active, int band_mod) {
-  __shared__ double2 cs[TR][TM];
-  __shared__ double2 ps[TM][AS];
+// grid (tiles, g chunks of 128), 128 threads; warp w covers g0 + 32 w .. + 32
+__global__ void __launch_bounds__(CW * 32) k_proj_apply(ProjArgs a, const double2* __restrict__ C,
+                                                        const double2* __restrict__ Xin,
+                                                        double2* __restrict__ Y, double ca,
+                                                        double cb, const int* __restrict__ active,
+                                                        int band_mod) {
   const ProjTile t = a.tiles[blockIdx.x];
-  const int g0 = blockIdx.y * AS;
   const int nocc = a.nocc[t.k];
   const double2* phi = a.phi + (size_t)a.off[t.k] * a.nbp;
-  const int tr = threadIdx.x >> 4, tg = threadIdx.x & 15;
-  double2 acc[4][4];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r4 = lane >> 2, c4 = lane & 3;
+  const int gw = blockIdx.y * AG + 32 * w;
+  double dr[2][4][2], di[2][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int jb = 0; jb < 2; ++jb)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
-
-  for (int mb = 0; mb < nocc; mb += TM) {
-    const int mlen = min(TM, nocc - mb);
-    for (int e = threadIdx.x; e < TR * TM; e += 128) {
-      const int r = e / TM, m = e - r * TM;
-      cs[r][m] = (r < t.nrows && m < mlen) ? C[(size_t)(t.row0 + r) * a.ldc + mb + m]
-                                           : make_double2(0.0, 0.0);
+    for (int gb = 0; gb < 4; ++gb) {
+      dr[jb][gb][0] = dr[jb][gb][1] = 0.0;
+      di[jb][gb][0] = di[jb][gb][1] = 0.0;
     }
-    for (int e = threadIdx.x; e < TM * AS; e += 128) {
-      const int m = e / AS, c = e - m * AS;
-      const int g = g0 + c;
-      ps[m][c] = (m < mlen && g < a.nbp) ? phi[(size_t)(mb + m) * a.nbp + g]
-                                         : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int m = 0; m < TM; ++m) {
-      double2 cv[4], pv[4];
+  if (gw < a.nbp) {
+    for (int m = 0; m < nocc; m += 4) {
+      const int mm = m + c4;
+      const bool mok = mm < nocc;
+      double2 av[2], bv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) cv[i] = cs[tr + 8 * i][m];
+      for (int jb = 0; jb < 2; ++jb) {
+        const int r = 8 * jb + r4;   // A[j = r4][k = c4] = C[row j][m + c4]
+        av[jb] = (mok && r < t.nrows) ? C[(size_t)(t.row0 + r) * a.ldc + mm]
+                                      : make_double2(0.0, 0.0);
+      }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) pv[j] = ps[m][tg + 16 * j];
+      for (int gb = 0; gb < 4; ++gb) {
+        const int g = gw + 8 * gb + r4;   // B[k = c4][n = r4] = Phi[m + c4][g]
+        bv[gb] = (mok && g < a.nbp) ? __ldg(&phi[(size_t)mm * a.nbp + g]) : make_double2(0.0, 0.0);
+      }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int jb = 0; jb < 2; ++jb)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc[i][j].x = fma(pv[j].x, cv[i].x, acc[i][j].x);
-          acc[i][j].x = fma(-pv[j].y, cv[i].y, acc[i][j].x);
-          acc[i][j].y = fma(pv[j].x, cv[i].y, acc[i][j].y);
-          acc[i][j].y = fma(pv[j].y, cv[i].x, acc[i][j].y);
+        for (int gb = 0; gb < 4; ++gb) {
+          // C * Phi : re = cr pr - ci pi ; im = cr pi + ci pr
+          dmma(dr[jb][gb][0], dr[jb][gb][1], av[jb].x, bv[gb].x);
+          dmma(dr[jb][gb][0], dr[jb][gb][1], -av[jb].y, bv[gb].y);
+          dmma(di[jb][gb][0], di[jb][gb][1], av[jb].x, bv[gb].y);
+          dmma(di[jb][gb][0], di[jb][gb][1], av[jb].y, bv[gb].x);
         }
     }
-    __syncthreads();
   }
+  // D fragment: row j = r4, g = 2 c4 + {0,1}
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = tr + 8 * i;
+  for (int jb = 0; jb < 2; ++jb) {
+    const int r = 8 * jb + r4;
     if (r >= t.nrows) continue;
-    const int row = t.row0 + r;
+    const int row = a.rows ? a.rows[t.row0 + r] : t.row0 + r;
     if (active && !active[row % band_mod]) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int g = g0 + tg + 16 * j;
-      if (g >= a.nbp) continue;
-      const size_t idx = (size_t)row * a.nbp + g;
-      double2 x = (ca != 0.0) ? Xin[idx] : make_double2(0.0, 0.0);
-      Y[idx] = make_double2(ca * x.x + cb * acc[i][j].x, ca * x.y + cb * acc[i][j].y);
-    }
+    for (int gb = 0; gb < 4; ++gb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int g = gw + 8 * gb + 2 * c4 + h;
+        if (g >= a.nbp) continue;
+        const size_t idx = (size_t)row * a.nbp + g;
+        const double2 x = (ca != 0.0) ? Xin[idx] : make_double2(0.0, 0.0);
+        Y[idx] = make_double2(ca * x.x + cb * dr[jb][gb][h], ca * x.y + cb * di[jb][gb][h]);
+      }
   }
 }
 
@@ -176,20 +222,30 @@ int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int
     i = j;
   }
   pl.nrows = n;
-  pl.mtiles = (maxocc + TM - 1) / TM;
+  pl.mtiles = (maxocc + CM - 1) / CM;
   const int ntiles = (int)pl.tiles.size();
-  int want = (2 * kSM + ntiles * pl.mtiles - 1) / std::max(1, ntiles * pl.mtiles);
-  int maxsplit = std::max(1, nbp / 64);
+  const int base = std::max(1, ntiles * pl.mtiles);
+  int want = (2 * kSM + base - 1) / base;
+  const int maxsplit = std::max(1, nbp / (16 * CW));
   pl.nsplit = std::min(std::max(1, want), maxsplit);
   int len = (nbp + pl.nsplit - 1) / pl.nsplit;
-  len = ((len + TS - 1) / TS) * TS;
+  len = ((len + 4 * CW - 1) / (4 * CW)) * (4 * CW);
   pl.split_len = len;
   pl.nsplit = (nbp + len - 1) / len;
-  PWB_TRY(pl.dtiles.ensure(pl.tiles.size() * sizeof(ProjTile)));
+  PWB_TRY(pl.dtiles.ensure(std::max<size_t>(1, pl.tiles.size()) * sizeof(ProjTile)));
   if (!pl.tiles.empty())
     PWB_CUDA(cudaMemcpy(pl.dtiles.ptr, pl.tiles.data(), pl.tiles.size() * sizeof(ProjTile),
                         cudaMemcpyHostToDevice));
+  const size_t ntm = (size_t)ntiles * pl.mtiles;
+  if (pl.counters.bytes < ntm * sizeof(unsigned) || !pl.counters.ptr) {
+    PWB_TRY(pl.counters.ensure(std::max<size_t>(1, ntm) * sizeof(unsigned)));
+    PWB_CUDA(cudaMemset(pl.counters.ptr, 0, std::max<size_t>(1, ntm) * sizeof(unsigned)));
+  }
   return PWB_OK;
+}
+
+size_t proj_part_elems(const ProjPlan& pl) {
+  return (size_t)pl.nsplit * pl.tiles.size() * pl.mtiles * CM * TR;
 }
 
 int proj_coeffs(const ProjPlan& pl, ProjArgs a, const double2* X, double2* part, double2* C,
@@ -198,14 +254,9 @@ int proj_coeffs(const ProjPlan& pl, ProjArgs a, const double2* X, double2* part,
   a.tiles = reinterpret_cast<const ProjTile*>(pl.dtiles.ptr);
   a.nrows_total = pl.nrows;
   dim3 grid((unsigned)pl.tiles.size(), pl.mtiles, pl.nsplit);
-  double2* target = (pl.nsplit == 1) ? C : part;
-  k_proj_partial<<<grid, 64, 0, st>>>(a, X, pl.split_len, target);
+  k_proj_coef<<<grid, CW * 32, 0, st>>>(a, X, pl.split_len, pl.nsplit, part, C,
+                                        reinterpret_cast<unsigned*>(pl.counters.ptr));
   PWB_LAUNCH_CHECK();
-  if (pl.nsplit > 1) {
-    const size_t n = (size_t)pl.nrows * a.ldc;
-    k_proj_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl.nsplit, n, part, C);
-    PWB_LAUNCH_CHECK();
-  }
   return PWB_OK;
 }
 
@@ -214,8 +265,8 @@ int proj_apply(const ProjPlan& pl, ProjArgs a, const double2* C, const double2* 
   if (pl.tiles.empty()) return PWB_OK;
   a.tiles = reinterpret_cast<const ProjTile*>(pl.dtiles.ptr);
   a.nrows_total = pl.nrows;
-  dim3 grid((unsigned)pl.tiles.size(), (a.nbp + AS - 1) / AS);
-  k_proj_apply<<<grid, 128, 0, st>>>(a, C, Xin, Y, ca, cb, active, band_mod > 0 ? band_mod : 1);
+  dim3 grid((unsigned)pl.tiles.size(), (a.nbp + AG - 1) / AG);
+  k_proj_apply<<<grid, CW * 32, 0, st>>>(a, C, Xin, Y, ca, cb, active, band_mod > 0 ? band_mod : 1);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }

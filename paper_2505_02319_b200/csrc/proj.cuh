@@ -22,15 +22,23 @@ struct ProjArgs {
   int nbp;
   int ldc;              // leading dim of C / partials (max nocc)
   int nrows_total;
+  const int* rows;      // optional: compact row i -> X row rows[i] (active-row compaction)
 };
 
 struct ProjPlan {
   std::vector<ProjTile> tiles;
   DevBuf dtiles;
+  DevBuf counters;   // split-K arrival counters (self-resetting)
   int nrows = 0, mtiles = 0, nsplit = 1, split_len = 0;
 };
 
 int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int>& nocc, int nbp);
+// scratch (complex elements) needed by proj_coeffs for this plan / any plan of <= nrows rows
+size_t proj_part_elems(const ProjPlan& pl);
+inline size_t proj_part_bound(int nrows, int ldc) {
+  const size_t mt = (size_t)(ldc + 31) / 32;
+  return (2 * (size_t)kSM + (size_t)nrows * mt + 64) * mt * 32 * 16 + 32 * 16;
+}
 // C = Phi^H X   (part: nsplit * nrows * ldc scratch)
 int proj_coeffs(const ProjPlan& pl, ProjArgs a, const double2* X, double2* part, double2* C,
                 cudaStream_t st);

@@ -91,9 +91,10 @@ __global__ void __launch_bounds__(NTC) k_cg_init2(GridDev g, CgScalars sc, int n
 __global__ void __launch_bounds__(NTC) k_cg_alpha(GridDev g, CgScalars sc, int n,
                                                   const double2* __restrict__ p,
                                                   const double2* __restrict__ ap,
-                                                  double2* __restrict__ xr) {
+                                                  double2* __restrict__ xr,
+                                                  const int* __restrict__ rows) {
   __shared__ double red[NTC / 32 + 1];
-  const int row = blockIdx.x;
+  const int row = rows ? rows[blockIdx.x] : blockIdx.x;
   if (!sc.active[row]) return;
   const double2* pp = p + (size_t)row * g.nbp;
   const double2* aa = ap + (size_t)row * g.nbp;
@@ -121,9 +122,10 @@ __global__ void __launch_bounds__(NTC) k_cg_alpha(GridDev g, CgScalars sc, int n
 // res = |r|; it++; converged / failed masking; z = M^-1 r for rows still active
 __global__ void __launch_bounds__(NTC) k_cg_resid(GridDev g, CgScalars sc, int n,
                                                   const double2* __restrict__ xr,
-                                                  double2* __restrict__ z) {
+                                                  double2* __restrict__ z,
+                                                  const int* __restrict__ rows) {
   __shared__ double red[NTC / 32 + 1];
-  const int row = blockIdx.x;
+  const int row = rows ? rows[blockIdx.x] : blockIdx.x;
   if (!sc.active[row]) return;
   const double2* r = xr + (size_t)(n + row) * g.nbp;
   double acc = 0.0;
@@ -153,9 +155,10 @@ __global__ void __launch_bounds__(NTC) k_cg_resid(GridDev g, CgScalars sc, int n
 __global__ void __launch_bounds__(NTC) k_cg_beta(GridDev g, CgScalars sc, int n,
                                                  const double2* __restrict__ xr,
                                                  const double2* __restrict__ z,
-                                                 double2* __restrict__ p) {
+                                                 double2* __restrict__ p,
+                                                 const int* __restrict__ rows) {
   __shared__ double red[NTC / 32 + 1];
-  const int row = blockIdx.x;
+  const int row = rows ? rows[blockIdx.x] : blockIdx.x;
   if (!sc.active[row]) return;
   const double2* r = xr + (size_t)(n + row) * g.nbp;
   const double2* zz = z + (size_t)row * g.nbp;
@@ -250,7 +253,8 @@ static int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands) {
   PWB_CUDA(cudaMemset(cg.ap.ptr, 0, n * row));
   PWB_CUDA(cudaMemset(cg.z.ptr, 0, n * row));
   const int nsp = std::max(cg.plan1.nsplit, cg.plan2.nsplit);
-  PWB_TRY(cg.part.ensure((size_t)nsp * 2 * n * st->ldc * sizeof(double2)));
+  (void)nsp;
+  PWB_TRY(cg.part.ensure(proj_part_bound(2 * n, st->ldc) * sizeof(double2)));
   PWB_TRY(cg.cmat.ensure((size_t)2 * n * st->ldc * sizeof(double2)));
   // scalars
   const size_t nd = 5 * (size_t)n, ni = 4 * (size_t)n + 2;
@@ -276,6 +280,11 @@ static int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands) {
   PWB_CUDA(cudaMemcpy(cg.s.pshift, ps.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   PWB_CUDA(cudaMemcpy(cg.s.row_k, rk.data(), n * sizeof(int), cudaMemcpyHostToDevice));
   if (!cg.h_counters) PWB_CUDA(cudaMallocHost(&cg.h_counters, 2 * sizeof(int)));
+  if (cg.h_active) cudaFreeHost(cg.h_active);
+  if (cg.h_rows) cudaFreeHost(cg.h_rows);
+  PWB_CUDA(cudaMallocHost(&cg.h_active, (size_t)n * sizeof(int)));
+  PWB_CUDA(cudaMallocHost(&cg.h_rows, 3 * (size_t)n * sizeof(int)));
+  PWB_TRY(cg.d_rows.ensure(3 * (size_t)n * sizeof(int)));
   return PWB_OK;
 }
 
@@ -288,18 +297,42 @@ static ProjArgs proj_args(pwb_state* st) {
   a.nbp = st->g->nbp;
   a.ldc = st->ldc;
   a.nrows_total = 0;
+  a.rows = nullptr;
   return a;
 }
 
-// Q X in place for rows of a plan (masked)
+// Q X in place for rows of a plan (masked); rows = optional compact row list
 static int project(pwb_state* st, CgBatch& cg, const ProjPlan& pl, double2* X, const int* active,
-                   int band_mod) {
+                   int band_mod, const int* rows = nullptr) {
   ProjArgs a = proj_args(st);
+  a.rows = rows;
   cudaStream_t s = st->g->stream;
   cudaEvent_t e = prof().begin(s);
   PWB_TRY(proj_coeffs(pl, a, X, as<double2>(cg.part), as<double2>(cg.cmat), s));
   PWB_TRY(proj_apply(pl, a, as<double2>(cg.cmat), X, X, 1.0, -1.0, active, band_mod, s));
   prof().end(PROF_Q, e, s, pl.nrows);
+  return PWB_OK;
+}
+
+// Active-row compaction: from the host copy of the active flags build the
+// ascending list of rows still iterating (and its (x; r) twin for the stacked
+// buffer), their k-grouped projector tiles, and upload both.  Converged rows
+// then cost nothing in the H apply, the projector GEMMs or the CG kernels.
+static int compact_rows(pwb_state* st, CgBatch& cg, int n, int& na) {
+  na = 0;
+  for (int i = 0; i < n; ++i)
+    if (cg.h_active[i]) cg.h_rows[na++] = i;
+  if (na == 0 || na == n) return PWB_OK;
+  for (int i = 0; i < na; ++i) {
+    cg.h_rows[na + i] = cg.h_rows[i];
+    cg.h_rows[2 * na + i] = cg.h_rows[i] + n;
+  }
+  std::vector<int> rk(na), rk2(2 * na);
+  for (int i = 0; i < na; ++i) rk[i] = rk2[i] = rk2[na + i] = st->band_k[cg.bands[cg.h_rows[i]]];
+  PWB_TRY(proj_plan(cg.plan_a, rk, st->nocc, st->g->nbp));
+  PWB_TRY(proj_plan(cg.plan_b, rk2, st->nocc, st->g->nbp));
+  PWB_CUDA(cudaMemcpyAsync(cg.d_rows.ptr, cg.h_rows, 3 * (size_t)na * sizeof(int),
+                           cudaMemcpyHostToDevice, st->g->stream));
   return PWB_OK;
 }
 
@@ -330,32 +363,42 @@ static int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, 
   double2* W = as<double2>(g->wbuf);
   const double* vloc = as<double>(st->vloc);
   bool failed = false;
+  for (int i = 0; i < n; ++i) cg.h_active[i] = 1;
   for (int it = 0;; ++it) {
-    PWB_TRY(project(st, cg, cg.plan1, p, cg.s.active, n));
+    int na = n;
+    PWB_TRY(compact_rows(st, cg, n, na));
+    const bool compact = na < n;
+    const int* rows = compact ? as<int>(cg.d_rows) : nullptr;
+    const int* rows2 = compact ? as<int>(cg.d_rows) + na : nullptr;
+    const ProjPlan& pa = compact ? cg.plan_a : cg.plan1;
+    const ProjPlan& pb = compact ? cg.plan_b : cg.plan2;
+    PWB_TRY(project(st, cg, pa, p, cg.s.active, n, rows));
     cudaEvent_t eh = prof().begin(s);
-    PWB_TRY(launch_plane_inv(g, n, bk, p, 1.0, W));
-    PWB_TRY(launch_pencil_vmul(g, n, W, vloc, 1.0 / g->ng));
-    PWB_TRY(launch_plane_fwd(g, n, bk, W, 1.0, p, cg.s.eps, ap));
-    prof().end(PROF_H, eh, s, n);
-    PWB_TRY(project(st, cg, cg.plan1, ap, cg.s.active, n));
+    PWB_TRY(launch_plane_inv(g, na, bk, p, 1.0, W, rows));
+    PWB_TRY(launch_pencil_vmul(g, na, W, vloc, 1.0 / g->ng));
+    PWB_TRY(launch_plane_fwd(g, na, bk, W, 1.0, p, cg.s.eps, ap, rows));
+    prof().end(PROF_H, eh, s, na);
+    PWB_TRY(project(st, cg, pa, ap, cg.s.active, n, rows));
     cudaEvent_t ec = prof().begin(s);
-    k_cg_alpha<<<n, NTC, 0, s>>>(g->dev, cg.s, n, p, ap, xr);
+    k_cg_alpha<<<na, NTC, 0, s>>>(g->dev, cg.s, n, p, ap, xr, rows);
     PWB_LAUNCH_CHECK();
-    prof().end(PROF_CG, ec, s, n);
-    PWB_TRY(project(st, cg, cg.plan2, xr, cg.s.active, n));
+    prof().end(PROF_CG, ec, s, na);
+    PWB_TRY(project(st, cg, pb, xr, cg.s.active, n, rows2));
     ec = prof().begin(s);
     k_zero_counters<<<1, 1, 0, s>>>(cg.s.counters);
     PWB_LAUNCH_CHECK();
-    k_cg_resid<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z);
+    k_cg_resid<<<na, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, rows);
     PWB_LAUNCH_CHECK();
-    prof().end(PROF_CG, ec, s, n);
+    prof().end(PROF_CG, ec, s, na);
     PWB_CUDA(cudaMemcpyAsync(cg.h_counters, cg.s.counters, 2 * sizeof(int),
                              cudaMemcpyDeviceToHost, s));
-    PWB_TRY(project(st, cg, cg.plan1, z, cg.s.active, n));
+    PWB_CUDA(cudaMemcpyAsync(cg.h_active, cg.s.active, n * sizeof(int), cudaMemcpyDeviceToHost,
+                             s));
+    PWB_TRY(project(st, cg, pa, z, cg.s.active, n, rows));
     ec = prof().begin(s);
-    k_cg_beta<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, p);
+    k_cg_beta<<<na, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, p, rows);
     PWB_LAUNCH_CHECK();
-    prof().end(PROF_CG, ec, s, n);
+    prof().end(PROF_CG, ec, s, na);
     PWB_CUDA(cudaStreamSynchronize(s));
     prof().flush();
     if (cg.h_counters[1]) failed = true;
@@ -510,8 +553,11 @@ int pwb_state_create(pwb_grid* g, const int* nocc_per_k, const double* kweight,
 int pwb_state_destroy(pwb_state* st) {
   if (!st) return PWB_OK;
   cudaDeviceSynchronize();
-  if (st->cg.h_counters) cudaFreeHost(st->cg.h_counters);
-  if (st->cg_user.h_counters) cudaFreeHost(st->cg_user.h_counters);
+  for (pwb::CgBatch* c : {&st->cg, &st->cg_user}) {
+    if (c->h_counters) cudaFreeHost(c->h_counters);
+    if (c->h_active) cudaFreeHost(c->h_active);
+    if (c->h_rows) cudaFreeHost(c->h_rows);
+  }
   delete st;
   return PWB_OK;
 }
@@ -532,7 +578,7 @@ int pwb_project_out(pwb_state* st, int k, int ncol, double* x) {
     st->user_plan_key = key;
   }
   CgBatch& cg = st->cg_user;
-  PWB_TRY(cg.part.ensure((size_t)st->user_plan.nsplit * ncol * st->ldc * sizeof(double2)));
+  PWB_TRY(cg.part.ensure(proj_part_elems(st->user_plan) * sizeof(double2)));
   PWB_TRY(cg.cmat.ensure((size_t)ncol * st->ldc * sizeof(double2)));
   return project(st, cg, st->user_plan, reinterpret_cast<double2*>(x), nullptr, ncol);
 }
@@ -712,7 +758,7 @@ int pwb_project_generic(int nb, int nocc, const double* phi, int ncol, double* x
   PWB_TRY(meta.ensure(2 * sizeof(int)));
   int hm[2] = {0, nocc};
   PWB_CUDA(cudaMemcpy(meta.ptr, hm, 2 * sizeof(int), cudaMemcpyHostToDevice));
-  PWB_TRY(part.ensure((size_t)plan.nsplit * ncol * nocc * sizeof(double2)));
+  PWB_TRY(part.ensure(proj_part_elems(plan) * sizeof(double2)));
   PWB_TRY(cmat.ensure((size_t)ncol * nocc * sizeof(double2)));
   ProjArgs a;
   a.phi = reinterpret_cast<const double2*>(phi);
@@ -722,6 +768,7 @@ int pwb_project_generic(int nb, int nocc, const double* phi, int ncol, double* x
   a.nbp = nb;
   a.ldc = nocc;
   a.nrows_total = ncol;
+  a.rows = nullptr;
   double2* X = reinterpret_cast<double2*>(x);
   PWB_TRY(proj_coeffs(plan, a, X, as<double2>(part), as<double2>(cmat), nullptr));
   PWB_TRY(proj_apply(plan, a, as<double2>(cmat), X, X, 1.0, -1.0, nullptr, ncol, nullptr));

@@ -32,6 +32,11 @@ struct CgBatch {
   DevBuf part, cmat;        // GEMM scratch
   CgScalars s;
   int* h_counters = nullptr;  // pinned
+  // active-row compaction (rebuilt every CG iteration)
+  int* h_active = nullptr;    // pinned copy of s.active
+  int* h_rows = nullptr;      // pinned: [na active rows][na rows][na rows + n]
+  DevBuf d_rows;
+  ProjPlan plan_a, plan_b;
 };
 
 // accumulation kernels (chi0.cu)
