@@ -24,8 +24,10 @@ __global__ void __launch_bounds__(NT) k_plane_inv(GridDev g, const double2* __re
                                                   const double2* __restrict__ psi2,
                                                   const int* __restrict__ band_k, double scale,
                                                   double2* __restrict__ W,
-                                                  const int* __restrict__ rows) {
+                                                  const int* __restrict__ rows,
+                                                  const int* __restrict__ nact) {
   extern __shared__ double2 sm[];
+  if (nact && (int)blockIdx.y >= *nact) return;   // device-side row count (graph replay)
   const int p = blockIdx.x;
   const int b = blockIdx.y;                     // plane-buffer slot
   const int row = rows ? rows[b] : b;           // sphere row (active-row compaction)
@@ -58,8 +60,10 @@ __global__ void __launch_bounds__(NT) k_plane_fwd(GridDev g, const double2* __re
                                                   const double2* __restrict__ psi_in,
                                                   const double* __restrict__ shift,
                                                   double2* __restrict__ out,
-                                                  const int* __restrict__ rows) {
+                                                  const int* __restrict__ rows,
+                                                  const int* __restrict__ nact) {
   extern __shared__ double2 sm[];
+  if (nact && (int)blockIdx.y >= *nact) return;
   const int p = blockIdx.x;
   const int slot = blockIdx.y;                  // plane-buffer slot
   const int b = rows ? rows[slot] : slot;       // sphere row
@@ -114,6 +118,7 @@ struct PencilArgs {
   const double* lda_v;    // optional: rout += lda_c * max(rho,1e-10)^(-2/3) * lda_v
   const double* lda_rho;
   double lda_c;
+  const int* nact;        // optional device row count: blocks with b >= *nact exit
 };
 
 template <int IN, int OUT, class FX>
@@ -122,6 +127,7 @@ __global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
   const int T = g.tile, Tp = g.tilep, nx = g.nx, nyz = g.nyz;
   const int t0 = blockIdx.x * T;
   const int b = blockIdx.y;
+  if (a.nact && b >= *a.nact) return;
   const int nt = min(T, nyz - t0);
   if (IN == 0) {
     if (a.nxin < nx) {
@@ -230,13 +236,13 @@ static int check_band_count(int n) {
 }
 
 int launch_plane_inv(pwb_grid* g, int nband, const int* band_k, const double2* psi, double scale,
-                     double2* W, const int* rows) {
+                     double2* W, const int* rows, const int* nact) {
   PWB_TRY(check_band_count(nband));
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
     k_plane_inv<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
-        g->dev, psi, nullptr, band_k, scale, W, rows);
+        g->dev, psi, nullptr, band_k, scale, W, rows, nact);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -249,20 +255,21 @@ int launch_plane_inv2(pwb_grid* g, int nband, const int* band_k, const double2* 
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
     k_plane_inv<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
-        g->dev, a, b, band_k, 1.0, W, nullptr);
+        g->dev, a, b, band_k, 1.0, W, nullptr, nullptr);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
 
 int launch_plane_fwd(pwb_grid* g, int nband, const int* band_k, const double2* W, double a,
-                     const double2* psi_in, const double* shift, double2* out, const int* rows) {
+                     const double2* psi_in, const double* shift, double2* out, const int* rows,
+                     const int* nact) {
   PWB_TRY(check_band_count(nband));
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
     k_plane_fwd<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
-        g->dev, W, band_k, a, psi_in, shift, out, rows);
+        g->dev, W, band_k, a, psi_in, shift, out, rows, nact);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -276,10 +283,12 @@ static PencilArgs empty_args() {
   return a;
 }
 
-int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, double vscale) {
+int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, double vscale,
+                       const int* nact) {
   PWB_TRY(check_band_count(nband));
   if (nband == 0) return PWB_OK;
   PencilArgs a = empty_args();
+  a.nact = nact;
   a.win = W;
   a.xin = g->dev.xa;
   a.nxin = g->nxa;

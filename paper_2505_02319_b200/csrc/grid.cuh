@@ -68,14 +68,16 @@ namespace pwb {
 
 // launchers (fft_kernels.cu); all asynchronous on grid->stream
 // rows (optional): plane-buffer slot b reads/writes sphere row rows[b] (active-row compaction)
+// nact (optional): device row count; grid rows >= *nact exit (fixed-grid graph replay)
 int launch_plane_inv(pwb_grid* g, int nband, const int* band_k, const double2* psi, double scale,
-                     double2* W, const int* rows = nullptr);
+                     double2* W, const int* rows = nullptr, const int* nact = nullptr);
 int launch_plane_inv2(pwb_grid* g, int nband, const int* band_k, const double2* a,
                       const double2* b, double2* W);
-int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, double vscale);
+int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, double vscale,
+                       const int* nact = nullptr);
 int launch_plane_fwd(pwb_grid* g, int nband, const int* band_k, const double2* W, double a,
                      const double2* psi_in, const double* shift, double2* out,
-                     const int* rows = nullptr);
+                     const int* rows = nullptr, const int* nact = nullptr);
 int launch_pencil_to_cube(pwb_grid* g, int nband, const double2* W, double scale, double2* out);
 int launch_pencil_from_cube(pwb_grid* g, int nband, const double2* in, double2* W);
 // full-cube (all planes) helpers

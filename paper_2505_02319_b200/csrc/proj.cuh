@@ -8,6 +8,8 @@
 
 namespace pwb {
 
+constexpr int kProjTileRows = 16;   // rows per projector tile (2 DMMA n-fragments)
+
 struct ProjTile {
   int row0;   // first row of X in this tile
   int nrows;  // <= 32, all in k block `k`
@@ -23,16 +25,40 @@ struct ProjArgs {
   int ldc;              // leading dim of C / partials (max nocc)
   int nrows_total;
   const int* rows;      // optional: compact row i -> X row rows[i] (active-row compaction)
+  const int* ntiles;    // optional device tile count: CTAs with blockIdx.x >= *ntiles exit
 };
 
 struct ProjPlan {
   std::vector<ProjTile> tiles;
   DevBuf dtiles;
   DevBuf counters;   // split-K arrival counters (self-resetting)
+  ProjTile* h_stage = nullptr;   // pinned staging for async tile uploads
+  size_t h_cap = 0;
   int nrows = 0, mtiles = 0, nsplit = 1, split_len = 0;
+  int max_tiles = 0;   // > 0: tiles are produced on the device (capacity plan)
+  ~ProjPlan() {
+    if (h_stage) cudaFreeHost(h_stage);
+  }
 };
 
-int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int>& nocc, int nbp);
+inline int plan_tiles(const ProjPlan& pl) {
+  return pl.max_tiles > 0 ? pl.max_tiles : (int)pl.tiles.size();
+}
+
+// fused one-launch Q (cluster of 8 CTAs per row tile, DSMEM reduction of C):
+// Y = ca X + cb Phi (Phi^H X), rows with active[row % band_mod] == 0 untouched
+int proj_q(const ProjPlan& pl, ProjArgs a, const double2* Xin, double2* Y, double ca, double cb,
+           const int* active, int band_mod, cudaStream_t st);
+
+// capacity plan whose tile list (<= max_tiles entries) is written on the device;
+// launches cover max_tiles and CTAs beyond the device count ProjArgs::ntiles exit
+int proj_plan_device(ProjPlan& pl, int max_tiles, int maxocc, int nbp);
+
+// build the tile list for rows with k blocks row_k; uploads synchronously, or
+// asynchronously on `st` when st != nullptr (staging buffer reused: the caller
+// must not rebuild the plan before that stream has passed the upload)
+int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int>& nocc, int nbp,
+              cudaStream_t st = nullptr, bool async = false);
 // scratch (complex elements) needed by proj_coeffs for this plan / any plan of <= nrows rows
 size_t proj_part_elems(const ProjPlan& pl);
 inline size_t proj_part_bound(int nrows, int ldc) {

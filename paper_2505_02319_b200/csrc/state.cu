@@ -21,168 +21,6 @@ namespace pwb {
 
 int configure_chi0_kernels(const pwb_grid* g);
 
-constexpr int NTC = 256;
-
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NTC / 32; ++i) s += red[i];
-    red[NTC / 32] = s;
-  }
-  __syncthreads();
-  return red[NTC / 32];
-}
-
-// minv_s = 1 / (kin_s + pshift)
-__device__ __forceinline__ double minv(const GridDev& g, int k, int s, double pshift) {
-  return 1.0 / (g.kin[(size_t)k * g.nbp + s] + pshift);
-}
-
-// x = 0, r = rhs, z = M^-1 r
-__global__ void __launch_bounds__(NTC) k_cg_init(GridDev g, CgScalars sc, int n,
-                                                 const double2* __restrict__ rhs,
-                                                 double2* __restrict__ xr, double2* __restrict__ z) {
-  const int row = blockIdx.x;
-  const int k = sc.row_k[row];
-  const double ps = sc.pshift[row];
-  double2* x = xr + (size_t)row * g.nbp;
-  double2* r = xr + (size_t)(n + row) * g.nbp;
-  double2* zz = z + (size_t)row * g.nbp;
-  const double2* b = rhs + (size_t)row * g.nbp;
-  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
-    const double2 v = b[s];
-    x[s] = make_double2(0.0, 0.0);
-    r[s] = v;
-    zz[s] = cscale(v, minv(g, k, s, ps));
-  }
-  if (threadIdx.x == 0) {
-    sc.active[row] = 1;
-    sc.iters[row] = 0;
-    sc.res[row] = 0.0;
-  }
-}
-
-// rz = Re<r, z>; p = z
-__global__ void __launch_bounds__(NTC) k_cg_init2(GridDev g, CgScalars sc, int n,
-                                                  const double2* __restrict__ xr,
-                                                  const double2* __restrict__ z,
-                                                  double2* __restrict__ p) {
-  __shared__ double red[NTC / 32 + 1];
-  const int row = blockIdx.x;
-  const double2* r = xr + (size_t)(n + row) * g.nbp;
-  const double2* zz = z + (size_t)row * g.nbp;
-  double2* pp = p + (size_t)row * g.nbp;
-  double acc = 0.0;
-  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
-    const double2 a = r[s], c = zz[s];
-    acc += a.x * c.x + a.y * c.y;
-    pp[s] = c;
-  }
-  const double rz = block_sum(acc, red);
-  if (threadIdx.x == 0) sc.rz[row] = rz;
-}
-
-// alpha = rz / Re<p, Ap> (0 if <= 0); x += alpha p; r -= alpha Ap   (active rows)
-__global__ void __launch_bounds__(NTC) k_cg_alpha(GridDev g, CgScalars sc, int n,
-                                                  const double2* __restrict__ p,
-                                                  const double2* __restrict__ ap,
-                                                  double2* __restrict__ xr,
-                                                  const int* __restrict__ rows) {
-  __shared__ double red[NTC / 32 + 1];
-  const int row = rows ? rows[blockIdx.x] : blockIdx.x;
-  if (!sc.active[row]) return;
-  const double2* pp = p + (size_t)row * g.nbp;
-  const double2* aa = ap + (size_t)row * g.nbp;
-  double acc = 0.0;
-  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
-    const double2 a = pp[s], c = aa[s];
-    acc += a.x * c.x + a.y * c.y;
-  }
-  const double pap = block_sum(acc, red);
-  const double alpha = pap > 0.0 ? sc.rz[row] / pap : 0.0;
-  double2* x = xr + (size_t)row * g.nbp;
-  double2* r = xr + (size_t)(n + row) * g.nbp;
-  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
-    const double2 a = pp[s], c = aa[s];
-    double2 xv = x[s], rv = r[s];
-    xv.x += alpha * a.x;
-    xv.y += alpha * a.y;
-    rv.x -= alpha * c.x;
-    rv.y -= alpha * c.y;
-    x[s] = xv;
-    r[s] = rv;
-  }
-}
-
-// res = |r|; it++; converged / failed masking; z = M^-1 r for rows still active
-__global__ void __launch_bounds__(NTC) k_cg_resid(GridDev g, CgScalars sc, int n,
-                                                  const double2* __restrict__ xr,
-                                                  double2* __restrict__ z,
-                                                  const int* __restrict__ rows) {
-  __shared__ double red[NTC / 32 + 1];
-  const int row = rows ? rows[blockIdx.x] : blockIdx.x;
-  if (!sc.active[row]) return;
-  const double2* r = xr + (size_t)(n + row) * g.nbp;
-  double acc = 0.0;
-  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
-    const double2 a = r[s];
-    acc += a.x * a.x + a.y * a.y;
-  }
-  const double res = sqrt(block_sum(acc, red));
-  const int it = sc.iters[row] + 1;
-  bool done = res <= sc.tol[row];
-  bool failed = !done && it >= sc.maxit[row];
-  if (threadIdx.x == 0) {
-    sc.res[row] = res;
-    sc.iters[row] = it;
-    if (done || failed) sc.active[row] = 0;
-    if (failed) atomicExch(&sc.counters[1], 1);
-    if (!done && !failed) atomicAdd(&sc.counters[0], 1);
-  }
-  if (done || failed) return;
-  const int k = sc.row_k[row];
-  const double ps = sc.pshift[row];
-  double2* zz = z + (size_t)row * g.nbp;
-  for (int s = threadIdx.x; s < g.nbp; s += NTC) zz[s] = cscale(r[s], minv(g, k, s, ps));
-}
-
-// rz' = Re<r, z>; beta = rz'/rz (0 if rz == 0); rz = rz'; p = z + beta p
-__global__ void __launch_bounds__(NTC) k_cg_beta(GridDev g, CgScalars sc, int n,
-                                                 const double2* __restrict__ xr,
-                                                 const double2* __restrict__ z,
-                                                 double2* __restrict__ p,
-                                                 const int* __restrict__ rows) {
-  __shared__ double red[NTC / 32 + 1];
-  const int row = rows ? rows[blockIdx.x] : blockIdx.x;
-  if (!sc.active[row]) return;
-  const double2* r = xr + (size_t)(n + row) * g.nbp;
-  const double2* zz = z + (size_t)row * g.nbp;
-  double acc = 0.0;
-  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
-    const double2 a = r[s], c = zz[s];
-    acc += a.x * c.x + a.y * c.y;
-  }
-  const double rzn = block_sum(acc, red);
-  const double rz = sc.rz[row];
-  const double beta = rz != 0.0 ? rzn / rz : 0.0;
-  double2* pp = p + (size_t)row * g.nbp;
-  for (int s = threadIdx.x; s < g.nbp; s += NTC) {
-    const double2 c = zz[s], q = pp[s];
-    pp[s] = make_double2(c.x + beta * q.x, c.y + beta * q.y);
-  }
-  if (threadIdx.x == 0) sc.rz[row] = rzn;
-}
-
-__global__ void k_zero_counters(int* c) {
-  c[0] = 0;
-  c[1] = 0;
-}
-
 // ---- chi0 helpers --------------------------------------------------------------
 // delta eps of local rows; fsum = sum w_k f'_n delta eps_n (fixed order, 1 CTA)
 __global__ void k_chi0_eps(int r0, int nrows, int ldc, const int* __restrict__ band_k,
@@ -228,204 +66,6 @@ __global__ void k_chi0_occ(int r0, int nrows, int ldc, const int* __restrict__ b
     c2[i] = coef[4 * band + 0];
     c1[i] = coef[4 * band + 3] * df;
   }
-}
-
-static int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands) {
-  pwb_grid* g = st->g;
-  const int n = (int)bands.size();
-  if (cg.nrows == n && cg.bands == bands) return PWB_OK;
-  cg.nrows = n;
-  cg.bands = bands;
-  std::vector<int> rk(n), rk2(2 * n);
-  for (int i = 0; i < n; ++i) {
-    if (bands[i] < 0 || bands[i] >= st->nband) return fail(PWB_ERR_VALUE, "band index out of range");
-    rk[i] = st->band_k[bands[i]];
-    rk2[i] = rk2[n + i] = rk[i];
-  }
-  PWB_TRY(proj_plan(cg.plan1, rk, st->nocc, g->nbp));
-  PWB_TRY(proj_plan(cg.plan2, rk2, st->nocc, g->nbp));
-  const size_t row = (size_t)g->nbp * sizeof(double2);
-  PWB_TRY(cg.xr.ensure(2 * n * row));
-  PWB_TRY(cg.z.ensure(n * row));
-  PWB_TRY(cg.p.ensure(n * row));
-  PWB_TRY(cg.ap.ensure(n * row));
-  PWB_TRY(cg.rhs.ensure(n * row));
-  PWB_CUDA(cudaMemset(cg.ap.ptr, 0, n * row));
-  PWB_CUDA(cudaMemset(cg.z.ptr, 0, n * row));
-  const int nsp = std::max(cg.plan1.nsplit, cg.plan2.nsplit);
-  (void)nsp;
-  PWB_TRY(cg.part.ensure(proj_part_bound(2 * n, st->ldc) * sizeof(double2)));
-  PWB_TRY(cg.cmat.ensure((size_t)2 * n * st->ldc * sizeof(double2)));
-  // scalars
-  const size_t nd = 5 * (size_t)n, ni = 4 * (size_t)n + 2;
-  PWB_TRY(cg.scal.ensure(nd * sizeof(double) + ni * sizeof(int)));
-  double* d = as<double>(cg.scal);
-  cg.s.rz = d;
-  cg.s.res = d + n;
-  cg.s.tol = d + 2 * n;
-  cg.s.eps = d + 3 * n;
-  cg.s.pshift = d + 4 * n;
-  int* ip = reinterpret_cast<int*>(d + nd);
-  cg.s.active = ip;
-  cg.s.iters = ip + n;
-  cg.s.maxit = ip + 2 * n;
-  cg.s.row_k = ip + 3 * n;
-  cg.s.counters = ip + 4 * n;
-  std::vector<double> eps(n), ps(n);
-  for (int i = 0; i < n; ++i) {
-    eps[i] = st->eps[bands[i]];
-    ps[i] = std::max(eps[i], 0.1);   // PRECONDITIONER_SHIFT_FLOOR (sternheimer.py:19)
-  }
-  PWB_CUDA(cudaMemcpy(cg.s.eps, eps.data(), n * sizeof(double), cudaMemcpyHostToDevice));
-  PWB_CUDA(cudaMemcpy(cg.s.pshift, ps.data(), n * sizeof(double), cudaMemcpyHostToDevice));
-  PWB_CUDA(cudaMemcpy(cg.s.row_k, rk.data(), n * sizeof(int), cudaMemcpyHostToDevice));
-  if (!cg.h_counters) PWB_CUDA(cudaMallocHost(&cg.h_counters, 2 * sizeof(int)));
-  if (cg.h_active) cudaFreeHost(cg.h_active);
-  if (cg.h_rows) cudaFreeHost(cg.h_rows);
-  PWB_CUDA(cudaMallocHost(&cg.h_active, (size_t)n * sizeof(int)));
-  PWB_CUDA(cudaMallocHost(&cg.h_rows, 3 * (size_t)n * sizeof(int)));
-  PWB_TRY(cg.d_rows.ensure(3 * (size_t)n * sizeof(int)));
-  return PWB_OK;
-}
-
-static ProjArgs proj_args(pwb_state* st) {
-  ProjArgs a;
-  a.phi = as<double2>(st->phi);
-  a.off = as<int>(st->d_off);
-  a.nocc = as<int>(st->d_nocc);
-  a.tiles = nullptr;
-  a.nbp = st->g->nbp;
-  a.ldc = st->ldc;
-  a.nrows_total = 0;
-  a.rows = nullptr;
-  return a;
-}
-
-// Q X in place for rows of a plan (masked); rows = optional compact row list
-static int project(pwb_state* st, CgBatch& cg, const ProjPlan& pl, double2* X, const int* active,
-                   int band_mod, const int* rows = nullptr) {
-  ProjArgs a = proj_args(st);
-  a.rows = rows;
-  cudaStream_t s = st->g->stream;
-  cudaEvent_t e = prof().begin(s);
-  PWB_TRY(proj_coeffs(pl, a, X, as<double2>(cg.part), as<double2>(cg.cmat), s));
-  PWB_TRY(proj_apply(pl, a, as<double2>(cg.cmat), X, X, 1.0, -1.0, active, band_mod, s));
-  prof().end(PROF_Q, e, s, pl.nrows);
-  return PWB_OK;
-}
-
-// Active-row compaction: from the host copy of the active flags build the
-// ascending list of rows still iterating (and its (x; r) twin for the stacked
-// buffer), their k-grouped projector tiles, and upload both.  Converged rows
-// then cost nothing in the H apply, the projector GEMMs or the CG kernels.
-static int compact_rows(pwb_state* st, CgBatch& cg, int n, int& na) {
-  na = 0;
-  for (int i = 0; i < n; ++i)
-    if (cg.h_active[i]) cg.h_rows[na++] = i;
-  if (na == 0 || na == n) return PWB_OK;
-  for (int i = 0; i < na; ++i) {
-    cg.h_rows[na + i] = cg.h_rows[i];
-    cg.h_rows[2 * na + i] = cg.h_rows[i] + n;
-  }
-  std::vector<int> rk(na), rk2(2 * na);
-  for (int i = 0; i < na; ++i) rk[i] = rk2[i] = rk2[na + i] = st->band_k[cg.bands[cg.h_rows[i]]];
-  PWB_TRY(proj_plan(cg.plan_a, rk, st->nocc, st->g->nbp));
-  PWB_TRY(proj_plan(cg.plan_b, rk2, st->nocc, st->g->nbp));
-  PWB_CUDA(cudaMemcpyAsync(cg.d_rows.ptr, cg.h_rows, 3 * (size_t)na * sizeof(int),
-                           cudaMemcpyHostToDevice, st->g->stream));
-  return PWB_OK;
-}
-
-// Run the batched PCG on cg.rhs with tolerances already in cg.s.tol.
-// On return x = rows [0, n) of cg.xr.
-static int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max_iter,
-                    int* iters_host, double* res_host) {
-  pwb_grid* g = st->g;
-  cudaStream_t s = g->stream;
-  const int n = cg.nrows;
-  if (n == 0) return PWB_OK;
-  std::vector<int> maxit(n);
-  for (int i = 0; i < n; ++i)
-    maxit[i] = max_iter > 0 ? max_iter : 10 * g->nb[st->band_k[cg.bands[i]]];
-  PWB_CUDA(cudaMemcpyAsync(cg.s.tol, tol.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
-  PWB_CUDA(cudaMemcpyAsync(cg.s.maxit, maxit.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
-  double2* xr = as<double2>(cg.xr);
-  double2* z = as<double2>(cg.z);
-  double2* p = as<double2>(cg.p);
-  double2* ap = as<double2>(cg.ap);
-  const int* bk = cg.s.row_k;
-  k_cg_init<<<n, NTC, 0, s>>>(g->dev, cg.s, n, as<double2>(cg.rhs), xr, z);
-  PWB_LAUNCH_CHECK();
-  PWB_TRY(project(st, cg, cg.plan1, z, nullptr, n));
-  k_cg_init2<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, p);
-  PWB_LAUNCH_CHECK();
-  PWB_TRY(g->wbuf.ensure((size_t)n * g->nxa * g->nyz * sizeof(double2)));
-  double2* W = as<double2>(g->wbuf);
-  const double* vloc = as<double>(st->vloc);
-  bool failed = false;
-  for (int i = 0; i < n; ++i) cg.h_active[i] = 1;
-  for (int it = 0;; ++it) {
-    int na = n;
-    PWB_TRY(compact_rows(st, cg, n, na));
-    const bool compact = na < n;
-    const int* rows = compact ? as<int>(cg.d_rows) : nullptr;
-    const int* rows2 = compact ? as<int>(cg.d_rows) + na : nullptr;
-    const ProjPlan& pa = compact ? cg.plan_a : cg.plan1;
-    const ProjPlan& pb = compact ? cg.plan_b : cg.plan2;
-    PWB_TRY(project(st, cg, pa, p, cg.s.active, n, rows));
-    cudaEvent_t eh = prof().begin(s);
-    PWB_TRY(launch_plane_inv(g, na, bk, p, 1.0, W, rows));
-    PWB_TRY(launch_pencil_vmul(g, na, W, vloc, 1.0 / g->ng));
-    PWB_TRY(launch_plane_fwd(g, na, bk, W, 1.0, p, cg.s.eps, ap, rows));
-    prof().end(PROF_H, eh, s, na);
-    PWB_TRY(project(st, cg, pa, ap, cg.s.active, n, rows));
-    cudaEvent_t ec = prof().begin(s);
-    k_cg_alpha<<<na, NTC, 0, s>>>(g->dev, cg.s, n, p, ap, xr, rows);
-    PWB_LAUNCH_CHECK();
-    prof().end(PROF_CG, ec, s, na);
-    PWB_TRY(project(st, cg, pb, xr, cg.s.active, n, rows2));
-    ec = prof().begin(s);
-    k_zero_counters<<<1, 1, 0, s>>>(cg.s.counters);
-    PWB_LAUNCH_CHECK();
-    k_cg_resid<<<na, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, rows);
-    PWB_LAUNCH_CHECK();
-    prof().end(PROF_CG, ec, s, na);
-    PWB_CUDA(cudaMemcpyAsync(cg.h_counters, cg.s.counters, 2 * sizeof(int),
-                             cudaMemcpyDeviceToHost, s));
-    PWB_CUDA(cudaMemcpyAsync(cg.h_active, cg.s.active, n * sizeof(int), cudaMemcpyDeviceToHost,
-                             s));
-    PWB_TRY(project(st, cg, pa, z, cg.s.active, n, rows));
-    ec = prof().begin(s);
-    k_cg_beta<<<na, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, p, rows);
-    PWB_LAUNCH_CHECK();
-    prof().end(PROF_CG, ec, s, na);
-    PWB_CUDA(cudaStreamSynchronize(s));
-    prof().flush();
-    if (cg.h_counters[1]) failed = true;
-    if (cg.h_counters[0] == 0) break;
-  }
-  std::vector<int> its(n);
-  std::vector<double> res(n);
-  PWB_CUDA(cudaMemcpyAsync(its.data(), cg.s.iters, n * sizeof(int), cudaMemcpyDeviceToHost, s));
-  PWB_CUDA(cudaMemcpyAsync(res.data(), cg.s.res, n * sizeof(double), cudaMemcpyDeviceToHost, s));
-  PWB_CUDA(cudaStreamSynchronize(s));
-  int first_fail = -1;
-  for (int i = 0; i < n; ++i) {
-    if (res[i] > tol[i]) {
-      if (first_fail < 0) first_fail = i;
-      its[i] = -1;
-    }
-    if (iters_host) iters_host[i] = its[i];
-    if (res_host) res_host[i] = res[i];
-  }
-  if (failed || first_fail >= 0) {
-    char buf[256];
-    snprintf(buf, sizeof(buf), "Sternheimer CG for band %d stalled at %.3e (target %.3e)",
-             first_fail >= 0 ? cg.bands[first_fail] : -1,
-             first_fail >= 0 ? res[first_fail] : 0.0, first_fail >= 0 ? tol[first_fail] : 0.0);
-    return fail(PWB_ERR_NONCONV, buf);
-  }
-  return PWB_OK;
 }
 
 // psi(r) cache for rows [b0, b1)
@@ -553,12 +193,7 @@ int pwb_state_create(pwb_grid* g, const int* nocc_per_k, const double* kweight,
 int pwb_state_destroy(pwb_state* st) {
   if (!st) return PWB_OK;
   cudaDeviceSynchronize();
-  for (pwb::CgBatch* c : {&st->cg, &st->cg_user}) {
-    if (c->h_counters) cudaFreeHost(c->h_counters);
-    if (c->h_active) cudaFreeHost(c->h_active);
-    if (c->h_rows) cudaFreeHost(c->h_rows);
-  }
-  delete st;
+  delete st;   // CgBatch / CgGroup destructors release streams and pinned buffers
   return PWB_OK;
 }
 
@@ -580,7 +215,8 @@ int pwb_project_out(pwb_state* st, int k, int ncol, double* x) {
   CgBatch& cg = st->cg_user;
   PWB_TRY(cg.part.ensure(proj_part_elems(st->user_plan) * sizeof(double2)));
   PWB_TRY(cg.cmat.ensure((size_t)ncol * st->ldc * sizeof(double2)));
-  return project(st, cg, st->user_plan, reinterpret_cast<double2*>(x), nullptr, ncol);
+  return project_rows(st, st->user_plan, reinterpret_cast<double2*>(x), nullptr, ncol, nullptr,
+                      as<double2>(cg.part), as<double2>(cg.cmat), st->g->stream);
 }
 
 int pwb_sternheimer(pwb_state* st, int nrhs, const int* band_host, const double* rhs,
@@ -769,9 +405,14 @@ int pwb_project_generic(int nb, int nocc, const double* phi, int ncol, double* x
   a.ldc = nocc;
   a.nrows_total = ncol;
   a.rows = nullptr;
+  a.ntiles = nullptr;
   double2* X = reinterpret_cast<double2*>(x);
-  PWB_TRY(proj_coeffs(plan, a, X, as<double2>(part), as<double2>(cmat), nullptr));
-  PWB_TRY(proj_apply(plan, a, as<double2>(cmat), X, X, 1.0, -1.0, nullptr, ncol, nullptr));
+  if (getenv("PWB_PROJ_FUSED")) {   // cluster/DSMEM one-launch variant (comparison)
+    PWB_TRY(proj_q(plan, a, X, X, 1.0, -1.0, nullptr, ncol, nullptr));
+  } else {
+    PWB_TRY(proj_coeffs(plan, a, X, as<double2>(part), as<double2>(cmat), nullptr));
+    PWB_TRY(proj_apply(plan, a, as<double2>(cmat), X, X, 1.0, -1.0, nullptr, ncol, nullptr));
+  }
   PWB_CUDA(cudaStreamSynchronize(nullptr));
   return PWB_OK;
 }

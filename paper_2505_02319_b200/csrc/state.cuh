@@ -22,22 +22,47 @@ struct CgScalars {
   int* counters;   // [0] active count, [1] failure flag
 };
 
+// Device-side iteration control written by the compaction kernel each CG
+// iteration: counts, the active-row lists and the projector tile lists.
+struct IterCtl {
+  int* hdr;        // [0] na, [1] tiles A, [2] tiles B, [3] active count, [4] fail flag
+  int* rows;       // [n]   active rows, ascending
+  int* rows2;      // [2n]  rows then rows + n (stacked (x; r) buffer)
+  ProjTile* ta;    // tiles over rows
+  ProjTile* tb;    // tiles over rows2
+};
+
 struct CgBatch {
   int nrows = 0;
   std::vector<int> bands;   // global band of each row
-  ProjPlan plan1;           // rows [0, n)
-  ProjPlan plan2;           // rows [0, 2n) for the stacked (x; r) buffer
+  ProjPlan plan1;           // rows [0, n) (init / RHS)
+  ProjPlan pa, pb;          // device-tile plans (compacted rows / stacked rows)
   DevBuf xr, z, p, ap, rhs;
   DevBuf scal;              // CgScalars storage
   DevBuf part, cmat;        // GEMM scratch
+  DevBuf ctl_buf;           // IterCtl storage
+  IterCtl ctl;
   CgScalars s;
-  int* h_counters = nullptr;  // pinned
-  // active-row compaction (rebuilt every CG iteration)
-  int* h_active = nullptr;    // pinned copy of s.active
-  int* h_rows = nullptr;      // pinned: [na active rows][na rows][na rows + n]
-  DevBuf d_rows;
-  ProjPlan plan_a, plan_b;
+  int* h_hdr = nullptr;     // pinned copy of ctl.hdr
+  int max_tiles = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  void* graph_w = nullptr;  // plane buffer captured in the graph
+  int prof_rows = 0;        // active rows of the running iteration (profiler units)
+  ~CgBatch();
 };
+
+constexpr int kMaxK = 128;  // k blocks handled by the device-side compaction
+
+// batched PCG (cg.cu)
+ProjArgs proj_args(pwb_state* st);
+int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* active, int band_mod,
+                 const int* rows, double2* part, double2* cmat, cudaStream_t s,
+                 const int* ntiles = nullptr);
+int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands);
+int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max_iter,
+             int* iters_host, double* res_host);
 
 // accumulation kernels (chi0.cu)
 int launch_drho_partial(pwb_grid* g, int nband, const double2* W, const double2* psir,

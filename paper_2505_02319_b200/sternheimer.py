@@ -63,7 +63,15 @@ def solve_sternheimer_many(gs, v_local, bands, rhs_rows, tols, max_iter=None):
     """
     torch = torch_mod()
     ds = _state_for(gs, v_local)
-    bands = np.ascontiguousarray(bands, dtype=np.int32)
+    bands = np.asarray(bands, dtype=np.int32)
+    order = np.argsort(ds.band_k[bands], kind="stable")   # the batch runs k-grouped
+    if np.any(order != np.arange(len(bands))):
+        rhs_rows = np.asarray(rhs_rows)
+        sol, res, its = solve_sternheimer_many(gs, v_local, bands[order], rhs_rows[order],
+                                               np.asarray(tols, dtype=float)[order], max_iter)
+        inv = np.argsort(order)
+        return sol[inv], res[inv], its[inv]
+    bands = np.ascontiguousarray(bands)
     tols = np.ascontiguousarray(tols, dtype=float)
     m = len(bands)
     rhs = ds.grid.pack(list(rhs_rows), ds.band_k[bands])
