@@ -396,7 +396,7 @@ static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s) {
   double2* part = as<double2>(cg.part);
   double2* cmat = as<double2>(cg.cmat);
   double2* W = as<double2>(g->wbuf);
-  const double* vloc = as<double>(st->vloc);
+  const double* vloc = as<double>(st->vloct);   // x-major copy (fused pencil multiply)
   const int* bk = cg.s.row_k;
   const int* nact = cg.ctl.hdr;
   const int* rows = cg.ctl.rows;

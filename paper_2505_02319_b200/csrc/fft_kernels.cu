@@ -33,12 +33,14 @@ __global__ void __launch_bounds__(NT) k_plane_inv(GridDev g, const double2* __re
   const int row = rows ? rows[b] : b;           // sphere row (active-row compaction)
   const int k = band_k ? band_k[row] : 0;
   const int nyz = g.nyz;
-  for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = make_double2(0.0, 0.0);
+  const int ny = FY::N ? FY::N : g.ny;
+  const int nyp = g.nyp;   // odd smem row stride: conflict-free y and z lines
+  for (int i = threadIdx.x; i < g.nz * nyp; i += NT) sm[i] = make_double2(0.0, 0.0);
   __syncthreads();
   const int s0 = g.xr[k * (g.nxa + 1) + p];
   const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
   const double2* src = psi + (size_t)row * g.nbp;
-  const int* pp = g.pp + (size_t)k * g.nbp;
+  const int* pp = g.ppp + (size_t)k * g.nbp;
   if (psi2) {
     const double2* src2 = psi2 + (size_t)row * g.nbp;
     for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(cadd(src[s], src2[s]), scale);
@@ -46,10 +48,13 @@ __global__ void __launch_bounds__(NT) k_plane_inv(GridDev g, const double2* __re
     for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(src[s], scale);
   }
   __syncthreads();
-  FZ::template run<NT>(g, sm, g.nya, g.ny, 0, g.ya, true);   // z lines of active y
-  FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, true);  // y lines, every z
+  FZ::template run<NT>(g, sm, g.nya, nyp, 0, g.ya, true);      // z lines of active y
+  FY::template run<NT>(g, sm, g.nz, 1, nyp, nullptr, true, 0);  // y lines, threads across lines
   double2* dst = W + ((size_t)b * g.nxa + p) * nyz;
-  for (int i = threadIdx.x; i < nyz; i += NT) dst[i] = sm[i];
+  for (int i = threadIdx.x; i < nyz; i += NT) {
+    const int z = i / ny;
+    dst[i] = sm[i + z * (nyp - ny)];
+  }
 }
 
 // plane pass, forward: W[b][p] -> sphere rows with epilogue
@@ -69,14 +74,19 @@ __global__ void __launch_bounds__(NT) k_plane_fwd(GridDev g, const double2* __re
   const int b = rows ? rows[slot] : slot;       // sphere row
   const int k = band_k ? band_k[b] : 0;
   const int nyz = g.nyz;
+  const int ny = FY::N ? FY::N : g.ny;
+  const int nyp = g.nyp;
   const double2* srcw = W + ((size_t)slot * g.nxa + p) * nyz;
-  for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = srcw[i];
+  for (int i = threadIdx.x; i < nyz; i += NT) {
+    const int z = i / ny;
+    sm[i + z * (nyp - ny)] = srcw[i];
+  }
   __syncthreads();
-  FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, false);  // y lines, every z
-  FZ::template run<NT>(g, sm, g.nya, g.ny, 0, g.ya, false);    // z lines of active y
+  FY::template run<NT>(g, sm, g.nz, 1, nyp, nullptr, false, 0);  // y lines, every z
+  FZ::template run<NT>(g, sm, g.nya, nyp, 0, g.ya, false);       // z lines of active y
   const int s0 = g.xr[k * (g.nxa + 1) + p];
   const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
-  const int* pp = g.pp + (size_t)k * g.nbp;
+  const int* pp = g.ppp + (size_t)k * g.nbp;
   const double* kin = g.kin + (size_t)k * g.nbp;
   double2* dst = out + (size_t)b * g.nbp;
   const double sh = shift ? shift[b] : 0.0;
@@ -124,15 +134,23 @@ struct PencilArgs {
 template <int IN, int OUT, class FX>
 __global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
   extern __shared__ double2 sm[];
-  const int T = g.tile, Tp = g.tilep, nx = g.nx, nyz = g.nyz;
+  const int T = g.tile, Tp = g.tilep, nyz = g.nyz;
+  const int nx = FX::N ? FX::N : g.nx;   // compile-time for the codelet sizes
   const int t0 = blockIdx.x * T;
   const int b = blockIdx.y;
   if (a.nact && b >= *a.nact) return;
   const int nt = min(T, nyz - t0);
   if (IN == 0) {
     if (a.nxin < nx) {
-      for (int i = threadIdx.x; i < nx * Tp; i += NT) sm[i] = make_double2(0.0, 0.0);
-      __syncthreads();
+      // zero only the x rows outside the (contiguous, wrapped) active range
+      const int x0 = a.xin[a.nxin - 1] + 1;
+      const int nz_rows = nx - a.nxin;
+      for (int i = threadIdx.x; i < nz_rows * Tp; i += NT) {
+        const int q = i / Tp, t = i - q * Tp;
+        int x = x0 + q;
+        if (x >= nx) x -= nx;
+        sm[x * Tp + t] = make_double2(0.0, 0.0);
+      }
     }
     const double2* src = a.win + (size_t)b * a.in_stride;
     for (int i = threadIdx.x; i < a.nxin * nt; i += NT) {
@@ -151,15 +169,8 @@ __global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
     FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, false);
   } else if (a.mode >= 2) {
     FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, true);
-    if (a.mode == 3) {
-      const double* vv = a.v + (size_t)t0 * nx;
-      for (int i = threadIdx.x; i < nt * nx; i += NT) {
-        const int t = i / nx, x = i - t * nx;
-        sm[x * Tp + t] = cscale(sm[x * Tp + t], vv[i] * a.vscale);
-      }
-      __syncthreads();
-      FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, false);
-    }
+    if (a.mode == 3)   // V(r)/n_g applied inside the first pass of the forward transform
+      FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, false, -1, a.v + t0, nyz, a.vscale);
   }
   if (OUT == 0) {
     double2* dst = a.wout + (size_t)b * a.out_stride;
@@ -199,15 +210,17 @@ __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restric
   const int x = blockIdx.x;
   const int v = blockIdx.y;
   const int nyz = g.nyz;
+  const int ny = FY::N ? FY::N : g.ny;
+  const int nyp = g.nyp;
   double2* pl = Wf + ((size_t)v * g.nx + x) * nyz;
-  for (int i = threadIdx.x; i < nyz; i += NT) sm[i] = pl[i];
+  for (int i = threadIdx.x; i < nyz; i += NT) sm[i + (i / ny) * (nyp - ny)] = pl[i];
   __syncthreads();
   if (mode == 0 && inverse) {
-    FZ::template run<NT>(g, sm, g.ny, g.ny, 1, nullptr, true);
-    FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, true);
+    FZ::template run<NT>(g, sm, g.ny, nyp, 1, nullptr, true);
+    FY::template run<NT>(g, sm, g.nz, 1, nyp, nullptr, true, 0);
   } else {
-    FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, false);
-    FZ::template run<NT>(g, sm, g.ny, g.ny, 1, nullptr, false);
+    FY::template run<NT>(g, sm, g.nz, 1, nyp, nullptr, false, 0);
+    FZ::template run<NT>(g, sm, g.ny, nyp, 1, nullptr, false);
   }
   if (mode != 0) {
     const double* g2 = g.g2w + (size_t)x * nyz;
@@ -216,16 +229,17 @@ __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restric
       double d;
       if (mode == 1) d = (q == 0.0) ? 0.0 : 4.0 * M_PI / q;
       else d = (q == 0.0) ? 1.0 : q / (q + param * param);
-      sm[i] = cscale(sm[i], d);
+      const int j = i + (i / ny) * (nyp - ny);
+      sm[j] = cscale(sm[j], d);
     }
     __syncthreads();
-    FZ::template run<NT>(g, sm, g.ny, g.ny, 1, nullptr, true);
-    FY::template run<NT>(g, sm, g.nz, 1, g.ny, nullptr, true);
+    FZ::template run<NT>(g, sm, g.ny, nyp, 1, nullptr, true);
+    FY::template run<NT>(g, sm, g.nz, 1, nyp, nullptr, true, 0);
   }
-  for (int i = threadIdx.x; i < nyz; i += NT) pl[i] = sm[i];
+  for (int i = threadIdx.x; i < nyz; i += NT) pl[i] = sm[i + (i / ny) * (nyp - ny)];
 }
 
-size_t plane_smem(const pwb_grid* g) { return (size_t)g->nyz * sizeof(double2); }
+size_t plane_smem(const pwb_grid* g) { return (size_t)g->nz * g->dev.nyp * sizeof(double2); }
 size_t pencil_smem(const pwb_grid* g) { return (size_t)g->nx * g->dev.tilep * sizeof(double2); }
 
 static int tiles(const pwb_grid* g) { return (g->nyz + g->dev.tile - 1) / g->dev.tile; }
@@ -283,6 +297,31 @@ static PencilArgs empty_args() {
   return a;
 }
 
+// vt[x * nyz + t] = v[t * nx + x]: the x-major copy of a real grid vector used
+// by the fused V(r) multiply of the pencil pass (coalesced loads)
+__global__ void k_transpose_v(int nx, int nyz, const double* __restrict__ v,
+                              double* __restrict__ vt) {
+  __shared__ double tile[32][33];
+  const int t0 = blockIdx.x * 32, x0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int t = t0 + i, x = x0 + threadIdx.x;
+    if (t < nyz && x < nx) tile[i][threadIdx.x] = v[(size_t)t * nx + x];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int x = x0 + i, t = t0 + threadIdx.x;
+    if (t < nyz && x < nx) vt[(size_t)x * nyz + t] = tile[threadIdx.x][i];
+  }
+}
+
+int launch_transpose_v(pwb_grid* g, const double* v, double* vt) {
+  dim3 grid((g->nyz + 31) / 32, (g->nx + 31) / 32);
+  k_transpose_v<<<grid, dim3(32, 8), 0, g->stream>>>(g->nx, g->nyz, v, vt);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+// v: x-major (launch_transpose_v) real multiplier
 int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, double vscale,
                        const int* nact) {
   PWB_TRY(check_band_count(nband));

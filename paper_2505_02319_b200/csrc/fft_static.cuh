@@ -78,10 +78,15 @@ struct Dft<6> {
 
 // One compile-time Stockham pass (radix R, sub-transform size NS) over whole
 // lines, one butterfly per thread per round.
+// vm (first pass only, optional): input element e of line l is multiplied by
+// vs * vm[e * vld + l] as it is loaded (fuses the pointwise V(r) product of
+// the H apply into the forward transform).
 template <int N, int R, int NS, int NT>
 __device__ __forceinline__ void spass(double2* __restrict__ s, int nlines, int es, int ls,
                                       const int* __restrict__ lbase,
-                                      const double2* __restrict__ tw, bool inv, bool line_major) {
+                                      const double2* __restrict__ tw, bool inv, bool line_major,
+                                      const double* __restrict__ vm = nullptr, int vld = 0,
+                                      double vs = 1.0) {
   constexpr int NBF = N / R;
   constexpr int LPR = (NT / NBF) > 0 ? (NT / NBF) : 1;   // whole lines per round
   constexpr int TWS = N / (NS * R);
@@ -118,6 +123,14 @@ __device__ __forceinline__ void spass(double2* __restrict__ s, int nlines, int e
       base = lbase ? lbase[l] : l * ls;
 #pragma unroll
       for (int r = 0; r < R; ++r) v[r] = s[base + (j + r * NBF) * es];
+      if (NS == 1 && vm) {
+        // multiplier stored element-major (vm[e * vld + l]): consecutive lines are
+        // consecutive threads, so these loads coalesce
+        const double* vl = vm + l;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          v[r] = cscale(v[r], vs * __ldg(&vl[(size_t)(j + r * NBF) * vld]));
+      }
     }
     __syncthreads();
     if (ok) {
@@ -140,15 +153,18 @@ template <int N, int NS>
 struct Passes<N, NS> {
   template <int NT>
   static __device__ __forceinline__ void run(double2*, int, int, int, const int*, const double2*,
-                                            bool, bool) {}
+                                            bool, bool, const double* = nullptr, int = 0,
+                                            double = 1.0) {}
 };
 
 template <int N, int NS, int R, int... Rest>
 struct Passes<N, NS, R, Rest...> {
   template <int NT>
   static __device__ __forceinline__ void run(double2* s, int nl, int es, int ls, const int* lb,
-                                            const double2* tw, bool inv, bool lm) {
-    spass<N, R, NS, NT>(s, nl, es, ls, lb, tw, inv, lm);
+                                            const double2* tw, bool inv, bool lm,
+                                            const double* vm = nullptr, int vld = 0,
+                                            double vs = 1.0) {
+    spass<N, R, NS, NT>(s, nl, es, ls, lb, tw, inv, lm, vm, vld, vs);
     Passes<N, NS * R, Rest...>::template run<NT>(s, nl, es, ls, lb, tw, inv, lm);
   }
 };
@@ -164,8 +180,11 @@ struct StaticPlan {
     static constexpr bool ok = true;                                                     \
     template <int NT>                                                                    \
     static __device__ __forceinline__ void run(double2* s, int nl, int es, int ls,       \
-                                              const int* lb, const double2* tw, bool inv) { \
-      Passes<N, 1, __VA_ARGS__>::template run<NT>(s, nl, es, ls, lb, tw, inv, es == 1);  \
+                                              const int* lb, const double2* tw, bool inv, \
+                                              int lm = -1, const double* vm = nullptr,  \
+                                              int vld = 0, double vs = 1.0) {           \
+      Passes<N, 1, __VA_ARGS__>::template run<NT>(s, nl, es, ls, lb, tw, inv,            \
+                                                  lm < 0 ? es == 1 : lm == 1, vm, vld, vs); \
     }                                                                                    \
   };
 PWB_PLAN(6, 6)
@@ -182,49 +201,79 @@ PWB_PLAN(320, 16, 4, 5)
 #undef PWB_PLAN
 
 // line-FFT policies used to template the transform kernels
+//   run(g, s, nlines, es, ls, lbase, inv, lm, vm, vld, vs)
+// lm: line mapping (-1 auto = along the line when es == 1, 0 across lines,
+// 1 along); vm/vld/vs: optional pointwise real multiplier applied to the
+// input (element e of line l times vs * vm[e * vld + l]).  N = the compile-time
+// length (0 for the runtime engine).
+template <int NT>
+__device__ __forceinline__ void premultiply(double2* s, int n, int nl, int es, int ls,
+                                            const double* vm, int vld, double vs) {
+  for (int i = threadIdx.x; i < nl * n; i += NT) {
+    const int l = i / n, e = i - l * n;
+    s[l * ls + e * es] = cscale(s[l * ls + e * es], vs * vm[(size_t)e * vld + l]);
+  }
+  __syncthreads();
+}
+
 struct DynX {
+  static constexpr int N = 0;
   template <int NT>
   static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
-                                            int ls, const int* lb, bool inv) {
+                                            int ls, const int* lb, bool inv, int = -1,
+                                            const double* vm = nullptr, int vld = 0,
+                                            double vs = 1.0) {
+    if (vm) premultiply<NT>(s, g.px.n, nl, es, ls, vm, vld, vs);
     fft_lines<NT>(s, g.px, nl, es, ls, lb, inv);
   }
 };
 struct DynY {
+  static constexpr int N = 0;
   template <int NT>
   static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
-                                            int ls, const int* lb, bool inv) {
+                                            int ls, const int* lb, bool inv, int = -1,
+                                            const double* = nullptr, int = 0, double = 1.0) {
     fft_lines<NT>(s, g.py, nl, es, ls, lb, inv);
   }
 };
 struct DynZ {
+  static constexpr int N = 0;
   template <int NT>
   static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
-                                            int ls, const int* lb, bool inv) {
+                                            int ls, const int* lb, bool inv, int = -1,
+                                            const double* = nullptr, int = 0, double = 1.0) {
     fft_lines<NT>(s, g.pz, nl, es, ls, lb, inv);
   }
 };
-template <int N>
+template <int NN>
 struct StX {
+  static constexpr int N = NN;
   template <int NT>
   static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
-                                            int ls, const int* lb, bool inv) {
-    StaticPlan<N>::template run<NT>(s, nl, es, ls, lb, g.px.tw, inv);
+                                            int ls, const int* lb, bool inv, int lm = -1,
+                                            const double* vm = nullptr, int vld = 0,
+                                            double vs = 1.0) {
+    StaticPlan<NN>::template run<NT>(s, nl, es, ls, lb, g.px.tw, inv, lm, vm, vld, vs);
   }
 };
-template <int N>
+template <int NN>
 struct StY {
+  static constexpr int N = NN;
   template <int NT>
   static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
-                                            int ls, const int* lb, bool inv) {
-    StaticPlan<N>::template run<NT>(s, nl, es, ls, lb, g.py.tw, inv);
+                                            int ls, const int* lb, bool inv, int lm = -1,
+                                            const double* = nullptr, int = 0, double = 1.0) {
+    StaticPlan<NN>::template run<NT>(s, nl, es, ls, lb, g.py.tw, inv, lm);
   }
 };
-template <int N>
+template <int NN>
 struct StZ {
+  static constexpr int N = NN;
   template <int NT>
   static __device__ __forceinline__ void run(const GridDev& g, double2* s, int nl, int es,
-                                            int ls, const int* lb, bool inv) {
-    StaticPlan<N>::template run<NT>(s, nl, es, ls, lb, g.pz.tw, inv);
+                                            int ls, const int* lb, bool inv, int lm = -1,
+                                            const double* = nullptr, int = 0, double = 1.0) {
+    StaticPlan<NN>::template run<NT>(s, nl, es, ls, lb, g.pz.tw, inv, lm);
   }
 };
 

@@ -159,8 +159,9 @@ int pwb_grid_create(int nx, int ny, int nz, double volume, int nk, const int* nb
   for (int i = 0; i < ny; ++i) yall[i] = i;
 
   g->xr_host.assign((size_t)nk * (g->nxa + 1), 0);
-  std::vector<int> pp((size_t)nk * g->nbp, 0);
+  std::vector<int> pp((size_t)nk * g->nbp, 0), ppp((size_t)nk * g->nbp, 0);
   std::vector<double> kin((size_t)nk * g->nbp, 0.0);
+  const int nyp = (ny % 2 == 0) ? ny + 1 : ny;
   size_t off = 0;
   for (int k = 0; k < nk; ++k) {
     int* xr = &g->xr_host[(size_t)k * (g->nxa + 1)];
@@ -172,6 +173,7 @@ int pwb_grid_create(int nx, int ny, int nz, double volume, int nk, const int* nb
       prev = gi[0];
       count[gi[0] - ixmin]++;
       pp[(size_t)k * g->nbp + s] = wrap(gi[2], nz) * ny + wrap(gi[1], ny);
+      ppp[(size_t)k * g->nbp + s] = wrap(gi[2], nz) * nyp + wrap(gi[1], ny);
       kin[(size_t)k * g->nbp + s] = 0.5 * g2_sphere[off + s];
     }
     xr[0] = 0;
@@ -205,6 +207,8 @@ int pwb_grid_create(int nx, int ny, int nz, double volume, int nk, const int* nb
   PWB_TRY(upload(g, yall.data(), yall.size(), &d.yall));
   PWB_TRY(upload(g, g->xr_host.data(), g->xr_host.size(), &d.xr));
   PWB_TRY(upload(g, pp.data(), pp.size(), &d.pp));
+  PWB_TRY(upload(g, ppp.data(), ppp.size(), &d.ppp));
+  d.nyp = nyp;
   PWB_TRY(upload(g, kin.data(), kin.size(), &d.kin));
   PWB_TRY(upload(g, g2w.data(), g2w.size(), &d.g2w));
   PWB_TRY(radix_plan(nx, d.px));
@@ -265,8 +269,10 @@ int pwb_ham_apply(pwb_grid* g, int nband, const int* band_k, const double* psi,
   PWB_TRY(g->wbuf.ensure((size_t)nband * g->nxa * g->nyz * sizeof(double2)));
   double2* W = as<double2>(g->wbuf);
   const double2* p = reinterpret_cast<const double2*>(psi);
+  PWB_TRY(g->vt.ensure((size_t)g->ng * sizeof(double)));
+  PWB_TRY(launch_transpose_v(g, v_local, as<double>(g->vt)));
   PWB_TRY(launch_plane_inv(g, nband, band_k, p, 1.0, W));
-  PWB_TRY(launch_pencil_vmul(g, nband, W, v_local, 1.0 / g->ng));
+  PWB_TRY(launch_pencil_vmul(g, nband, W, as<double>(g->vt), 1.0 / g->ng));
   PWB_TRY(launch_plane_fwd(g, nband, band_k, W, 1.0, p, shift, reinterpret_cast<double2*>(out)));
   return PWB_OK;
 }

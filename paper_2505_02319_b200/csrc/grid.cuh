@@ -27,6 +27,8 @@ struct GridDev {
   const int* yall;  // [ny]
   const int* xr;    // [nk][nxa+1] sphere offsets of plane p
   const int* pp;    // [nk][nbp]   in-plane index iz*ny+iy of each sphere point
+  const int* ppp;   // [nk][nbp]   same in the padded smem plane: iz*nyp+iy
+  int nyp;          // smem plane row stride: ny rounded up to odd (bank-conflict free)
   const double* kin;  // [nk][nbp] |G+k|^2 / 2
   const double* g2w;  // [nx][nz][ny] |G|^2 in plane layout (full cube)
   LinePlan px, py, pz;
@@ -62,6 +64,7 @@ struct pwb_grid {
   pwb::DevBuf tmp_real;   // scratch real vectors
   pwb::DevBuf red;        // reduction scratch
   pwb::DevBuf scratch;    // small device scalars (GMRES)
+  pwb::DevBuf vt;         // x-major copy of a real multiplier (pencil V product)
 };
 
 namespace pwb {
@@ -73,8 +76,10 @@ int launch_plane_inv(pwb_grid* g, int nband, const int* band_k, const double2* p
                      double2* W, const int* rows = nullptr, const int* nact = nullptr);
 int launch_plane_inv2(pwb_grid* g, int nband, const int* band_k, const double2* a,
                       const double2* b, double2* W);
+// v must be x-major (launch_transpose_v)
 int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, double vscale,
                        const int* nact = nullptr);
+int launch_transpose_v(pwb_grid* g, const double* v, double* vt);
 int launch_plane_fwd(pwb_grid* g, int nband, const int* band_k, const double2* W, double a,
                      const double2* psi_in, const double* shift, double2* out,
                      const int* rows = nullptr, const int* nact = nullptr);

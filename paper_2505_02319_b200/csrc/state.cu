@@ -181,6 +181,8 @@ int pwb_state_create(pwb_grid* g, const int* nocc_per_k, const double* kweight,
   PWB_TRY(st->vloc.ensure((size_t)g->ng * sizeof(double)));
   PWB_TRY(st->rho.ensure((size_t)g->ng * sizeof(double)));
   PWB_CUDA(cudaMemcpy(st->vloc.ptr, v_local, (size_t)g->ng * sizeof(double), cudaMemcpyHostToDevice));
+  PWB_TRY(st->vloct.ensure((size_t)g->ng * sizeof(double)));
+  PWB_TRY(launch_transpose_v(g, as<double>(st->vloc), as<double>(st->vloct)));
   if (rho)
     PWB_CUDA(cudaMemcpy(st->rho.ptr, rho, (size_t)g->ng * sizeof(double), cudaMemcpyHostToDevice));
   else
@@ -267,8 +269,10 @@ int pwb_chi0_begin(pwb_state* st, int b0, int b1, const double* dv, double* fsum
   const int* bk = as<int>(st->d_band_k) + b0;
   double2* dvpsi = as<double2>(st->dvpsi);
   cudaEvent_t er = prof().begin(s);
+  PWB_TRY(g->vt.ensure((size_t)g->ng * sizeof(double)));
+  PWB_TRY(launch_transpose_v(g, dv, as<double>(g->vt)));
   PWB_TRY(launch_plane_inv(g, n, bk, phi, 1.0, W));
-  PWB_TRY(launch_pencil_vmul(g, n, W, dv, 1.0 / g->ng));
+  PWB_TRY(launch_pencil_vmul(g, n, W, as<double>(g->vt), 1.0 / g->ng));
   PWB_TRY(launch_plane_fwd(g, n, bk, W, 1.0, nullptr, nullptr, dvpsi));
   prof().end(PROF_RHS, er, s, n);
   // M^T = (Phi^H dvpsi)^T  (response.py:129)
