@@ -3,11 +3,16 @@
 // sternheimer.py:28-30 and response.py:129,138.
 //
 //   coef :  C[row][m] = sum_g conj(Phi_k[m][g]) X[row][g]
-//           split-K over the sphere (grid covers the 148 SMs); warps of a CTA
-//           reduce in smem, CTAs reduce through a partial buffer in FIXED
-//           split order by the last CTA to finish (threadfence + counter):
-//           bitwise reproducible, one launch.
+//           split-K over the sphere; warps of a CTA reduce in smem, splits are
+//           reduced in FIXED split order by the last CTA to finish a tile
+//           (threadfence + arrival counter): bitwise reproducible, one launch.
 //   apply:  Y[row][g] = a X[row][g] + b sum_m Phi_k[m][g] C[row][m]
+//
+// Both kernels are persistent over a work-item list ((tile, m block, split)
+// and (tile, g chunk)) with the grid sized to the SMs, and the number of
+// splits is chosen on the device from the live tile count: with active-row
+// compaction the tile count shrinks every CG iteration, and a fixed grid of
+// mostly-exiting CTAs (or too few splits) was measured to dominate the tail.
 //
 // Complex products are four real DMMAs (re.re, im.im, re.im, im.re).  Rows of
 // X are grouped in tiles of <= 16 rows sharing one k block; with active-row
@@ -23,194 +28,201 @@ constexpr int TR = kProjTileRows;   // rows per tile (2 DMMA n-fragments)
 constexpr int CM = 32;   // m per coef block (4 DMMA m-fragments)
 constexpr int CW = 8;    // warps per coef CTA
 constexpr int AW = 8;    // warps per apply CTA
-constexpr int AG = AW * 32;  // g per apply CTA (32 per warp)
+constexpr int AG = AW * 32;  // g per apply work item (32 per warp)
+constexpr int kCoefCtas = 2 * kSM;
+constexpr int kApplyCtas = 2 * kSM;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ int xrow(const ProjArgs& a, const ProjTile& t, int r) {
-  return a.rows ? a.rows[t.row0 + r] : t.row0 + r;
+// live split count for `units` (tile x m block) work units
+__device__ __forceinline__ int live_nsplit(int units, int nsplit_max) {
+  int s = (kCoefCtas + units - 1) / max(units, 1);
+  return max(1, min(s, nsplit_max));
 }
 
-// grid (tiles, m blocks, splits), 128 threads
 __global__ void __launch_bounds__(CW * 32) k_proj_coef(ProjArgs a, const double2* __restrict__ X,
-                                                       int split_len, int nsplit,
-                                                       double2* __restrict__ part,
+                                                       int nt_host, int tile_cap, int mtiles,
+                                                       int nsplit_max, double2* __restrict__ part,
                                                        double2* __restrict__ C,
                                                        unsigned* __restrict__ counters) {
   __shared__ double2 red[CW / 2][CM][TR];
   __shared__ bool last;
-  if (a.ntiles && (int)blockIdx.x >= *a.ntiles) return;   // device tile count (graph replay)
-  const ProjTile t = a.tiles[blockIdx.x];
-  const int m0 = blockIdx.y * CM;
-  const int nocc = a.nocc[t.k];
-  if (m0 >= nocc) return;
-  const int split = blockIdx.z;
-  const int g0 = split * split_len;
-  const int g1 = min(a.nbp, g0 + split_len);
-  const double2* phi = a.phi + (size_t)a.off[t.k] * a.nbp;
+  const int ntiles = a.ntiles ? *a.ntiles : nt_host;
+  const int units = ntiles * mtiles;
+  const int nsplit = live_nsplit(units, nsplit_max);
+  int split_len = (a.nbp + nsplit - 1) / nsplit;
+  split_len = ((split_len + 4 * CW - 1) / (4 * CW)) * (4 * CW);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r4 = lane >> 2, c4 = lane & 3;
-  // fragment source rows
-  const double2* prow[4];
-  bool pok[4];
+  const size_t stride = (size_t)tile_cap * mtiles * (CM * TR);   // per split
+  for (int item = blockIdx.x; item < units * nsplit; item += gridDim.x) {
+    const int split = item % nsplit;
+    const int unit = item / nsplit;
+    const int mblk = unit % mtiles, tile = unit / mtiles;
+    const ProjTile t = a.tiles[tile];
+    const int m0 = mblk * CM;
+    const int nocc = a.nocc[t.k];
+    if (m0 >= nocc) continue;   // uniform over the CTA
+    const int g0 = split * split_len;
+    const int g1 = min(a.nbp, g0 + split_len);
+    const double2* phi = a.phi + (size_t)a.off[t.k] * a.nbp;
+    const double2* prow[4];
+    bool pok[4];
 #pragma unroll
-  for (int ma = 0; ma < 4; ++ma) {
-    const int m = m0 + 8 * ma + r4;
-    pok[ma] = m < nocc;
-    prow[ma] = phi + (size_t)(pok[ma] ? m : 0) * a.nbp;
-  }
-  const double2* xrw[2];
-  bool xok[2];
-#pragma unroll
-  for (int nb = 0; nb < 2; ++nb) {
-    const int r = 8 * nb + r4;
-    xok[nb] = r < t.nrows;
-    xrw[nb] = X + (size_t)(xok[nb] ? xrow(a, t, r) : 0) * a.nbp;
-  }
-  double cr[4][2][2], ci[4][2][2];
-#pragma unroll
-  for (int ma = 0; ma < 4; ++ma)
+    for (int ma = 0; ma < 4; ++ma) {
+      const int m = m0 + 8 * ma + r4;
+      pok[ma] = m < nocc;
+      prow[ma] = phi + (size_t)(pok[ma] ? m : 0) * a.nbp;
+    }
+    const double2* xrw[2];
+    bool xok[2];
 #pragma unroll
     for (int nb = 0; nb < 2; ++nb) {
-      cr[ma][nb][0] = cr[ma][nb][1] = 0.0;
-      ci[ma][nb][0] = ci[ma][nb][1] = 0.0;
+      const int r = 8 * nb + r4;
+      xok[nb] = r < t.nrows;
+      xrw[nb] = X + (size_t)(xok[nb] ? (a.rows ? a.rows[t.row0 + r] : t.row0 + r) : 0) * a.nbp;
     }
-  // register double buffering: the next k-step's fragments are in flight while
-  // the current step's 32 DMMAs issue (ncu: the unpipelined loop was
-  // long_scoreboard-bound at <1% FP64 pipe use)
-  // batched prefetch: the fragments of NP k-steps are loaded before any is
-  // used, so each warp keeps NP*6 16-byte loads in flight (ncu: the one-step
-  // loop was long_scoreboard-bound at <1% FP64 pipe use)
-  constexpr int NP = 4;
-  for (int gb = g0 + 4 * w; gb < g1; gb += 4 * CW * NP) {
-    double2 av[NP][4], bv[NP][2];
-#pragma unroll
-    for (int u = 0; u < NP; ++u) {
-      const int gg = gb + 4 * CW * u + c4;
-      const bool gok = gg < g1;
-#pragma unroll
-      for (int ma = 0; ma < 4; ++ma)
-        av[u][ma] = (gok && pok[ma]) ? __ldg(&prow[ma][gg]) : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb)
-        bv[u][nb] = (gok && xok[nb]) ? xrw[nb][gg] : make_double2(0.0, 0.0);
-    }
-    // conj(phi) * x : re = pr xr + pi xi ; im = pr xi - pi xr.  Issued part-major
-    // so consecutive DMMAs hit 16 independent accumulator chains.
-#pragma unroll
-    for (int u = 0; u < NP; ++u) {
-#pragma unroll
-      for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb) {
-          dmma(cr[ma][nb][0], cr[ma][nb][1], av[u][ma].x, bv[u][nb].x);
-          dmma(ci[ma][nb][0], ci[ma][nb][1], av[u][ma].x, bv[u][nb].y);
-        }
-#pragma unroll
-      for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb) {
-          dmma(cr[ma][nb][0], cr[ma][nb][1], av[u][ma].y, bv[u][nb].y);
-          dmma(ci[ma][nb][0], ci[ma][nb][1], -av[u][ma].y, bv[u][nb].x);
-        }
-    }
-  }
-  // D fragment: (m = r4, row = 2 c4 + {0,1}) of each (ma, nb) tile.
-  // Fixed-order warp reduction in two halves (smem holds CW/2 tiles):
-  // warp w (< CW/2) adds warp w + CW/2, then the CW/2 sums are added in order.
-  if (w >= CW / 2) {
+    double cr[4][2][2], ci[4][2][2];
 #pragma unroll
     for (int ma = 0; ma < 4; ++ma)
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb)
+      for (int nb = 0; nb < 2; ++nb) {
+        cr[ma][nb][0] = cr[ma][nb][1] = 0.0;
+        ci[ma][nb][0] = ci[ma][nb][1] = 0.0;
+      }
+    // batched prefetch: the fragments of NP k-steps are loaded before any is used
+    constexpr int NP = 4;
+    for (int gb = g0 + 4 * w; gb < g1; gb += 4 * CW * NP) {
+      double2 av[NP][4], bv[NP][2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-          red[w - CW / 2][8 * ma + r4][8 * nb + 2 * c4 + h] =
-              make_double2(cr[ma][nb][h], ci[ma][nb][h]);
-  }
-  __syncthreads();
-  if (w < CW / 2) {
+      for (int u = 0; u < NP; ++u) {
+        const int gg = gb + 4 * CW * u + c4;
+        const bool gok = gg < g1;
 #pragma unroll
-    for (int ma = 0; ma < 4; ++ma)
+        for (int ma = 0; ma < 4; ++ma)
+          av[u][ma] = (gok && pok[ma]) ? __ldg(&prow[ma][gg]) : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb)
+        for (int nb = 0; nb < 2; ++nb)
+          bv[u][nb] = (gok && xok[nb]) ? xrw[nb][gg] : make_double2(0.0, 0.0);
+      }
+      // conj(phi) * x : re = pr xr + pi xi ; im = pr xi - pi xr (part-major issue)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double2& slot = red[w][8 * ma + r4][8 * nb + 2 * c4 + h];
-          slot = make_double2(cr[ma][nb][h] + slot.x, ci[ma][nb][h] + slot.y);
+      for (int u = 0; u < NP; ++u) {
+#pragma unroll
+        for (int ma = 0; ma < 4; ++ma)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb) {
+            dmma(cr[ma][nb][0], cr[ma][nb][1], av[u][ma].x, bv[u][nb].x);
+            dmma(ci[ma][nb][0], ci[ma][nb][1], av[u][ma].x, bv[u][nb].y);
+          }
+#pragma unroll
+        for (int ma = 0; ma < 4; ++ma)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb) {
+            dmma(cr[ma][nb][0], cr[ma][nb][1], av[u][ma].y, bv[u][nb].y);
+            dmma(ci[ma][nb][0], ci[ma][nb][1], -av[u][ma].y, bv[u][nb].x);
+          }
+      }
+    }
+    // fixed-order warp reduction in two halves: warp w (< CW/2) adds w + CW/2
+    if (w >= CW / 2) {
+#pragma unroll
+      for (int ma = 0; ma < 4; ++ma)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            red[w - CW / 2][8 * ma + r4][8 * nb + 2 * c4 + h] =
+                make_double2(cr[ma][nb][h], ci[ma][nb][h]);
+    }
+    __syncthreads();
+    if (w < CW / 2) {
+#pragma unroll
+      for (int ma = 0; ma < 4; ++ma)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double2& slot = red[w][8 * ma + r4][8 * nb + 2 * c4 + h];
+            slot = make_double2(cr[ma][nb][h] + slot.x, ci[ma][nb][h] + slot.y);
+          }
+    }
+    __syncthreads();
+    const size_t tile_id = (size_t)tile * mtiles + mblk;
+    double2* mypart = part + (size_t)split * stride + tile_id * (CM * TR);
+    for (int i = threadIdx.x; i < CM * TR; i += CW * 32) {
+      const int m = i / TR, r = i - m * TR;
+      double2 s = red[0][m][r];
+#pragma unroll
+      for (int q = 1; q < CW / 2; ++q) s = cadd(s, red[q][m][r]);
+      if (nsplit == 1) {
+        if (r < t.nrows && m0 + m < nocc) C[(size_t)(t.row0 + r) * a.ldc + m0 + m] = s;
+      } else {
+        mypart[i] = s;
+      }
+    }
+    if (nsplit > 1) {
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&counters[tile_id], 1u);
+        last = (prev == (unsigned)nsplit - 1);
+      }
+      __syncthreads();
+      if (last) {
+        __threadfence();
+        const double2* p0 = part + tile_id * (CM * TR);
+        for (int i = threadIdx.x; i < CM * TR; i += CW * 32) {
+          const int m = i / TR, r = i - m * TR;
+          double2 s = __ldcg(&p0[i]);
+          int q = 1;
+          // loads issued 8 at a time (serialised on L2 latency otherwise), summed in order
+          for (; q + 8 <= nsplit; q += 8) {
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(&p0[(size_t)(q + u) * stride + i]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s = cadd(s, v[u]);
+          }
+          for (; q < nsplit; ++q) s = cadd(s, __ldcg(&p0[(size_t)q * stride + i]));
+          if (r < t.nrows && m0 + m < nocc) C[(size_t)(t.row0 + r) * a.ldc + m0 + m] = s;
         }
-  }
-  __syncthreads();
-  // fixed-order sum over warp pairs -> this split's partial
-  const size_t tile_id = (size_t)blockIdx.x * gridDim.y + blockIdx.y;
-  double2* mypart = part + ((size_t)split * gridDim.x * gridDim.y + tile_id) * (CM * TR);
-  for (int i = threadIdx.x; i < CM * TR; i += CW * 32) {
-    const int m = i / TR, r = i - m * TR;
-    double2 s = red[0][m][r];
-#pragma unroll
-    for (int q = 1; q < CW / 2; ++q) s = cadd(s, red[q][m][r]);
-    if (nsplit == 1) {
-      if (r < t.nrows && m0 + m < nocc) C[(size_t)(t.row0 + r) * a.ldc + m0 + m] = s;
-    } else {
-      mypart[i] = s;
+        if (threadIdx.x == 0) counters[tile_id] = 0u;
+      }
     }
+    __syncthreads();   // red / last reused by the next item
   }
-  if (nsplit == 1) return;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&counters[tile_id], 1u);
-    last = (prev == (unsigned)nsplit - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const size_t stride = (size_t)gridDim.x * gridDim.y * (CM * TR);
-  const double2* p0 = part + tile_id * (CM * TR);
-  for (int i = threadIdx.x; i < CM * TR; i += CW * 32) {
-    const int m = i / TR, r = i - m * TR;
-    double2 s = p0[i];
-    int q = 1;
-    // loads issued 8 at a time (they were serialised on L2 latency), summed in order
-    for (; q + 8 <= nsplit; q += 8) {
-      double2 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(&p0[(size_t)(q + u) * stride + i]);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s = cadd(s, v[u]);
-    }
-    for (; q < nsplit; ++q) s = cadd(s, __ldcg(&p0[(size_t)q * stride + i]));
-    if (r < t.nrows && m0 + m < nocc) C[(size_t)(t.row0 + r) * a.ldc + m0 + m] = s;
-  }
-  if (threadIdx.x == 0) counters[tile_id] = 0u;
 }
 
-// grid (tiles, g chunks of AG), AW warps; warp w covers g0 + 32 w .. + 32
+// work item = (tile, chunk of AG g); warp w covers g0 + 32 w .. + 32
 __global__ void __launch_bounds__(AW * 32) k_proj_apply(ProjArgs a, const double2* __restrict__ C,
                                                         const double2* __restrict__ Xin,
                                                         double2* __restrict__ Y, double ca,
                                                         double cb, const int* __restrict__ active,
-                                                        int band_mod) {
-  if (a.ntiles && (int)blockIdx.x >= *a.ntiles) return;   // device tile count (graph replay)
-  const ProjTile t = a.tiles[blockIdx.x];
-  const int nocc = a.nocc[t.k];
-  const double2* phi = a.phi + (size_t)a.off[t.k] * a.nbp;
+                                                        int band_mod, int nt_host) {
+  const int ntiles = a.ntiles ? *a.ntiles : nt_host;
+  const int nchunk = (a.nbp + AG - 1) / AG;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r4 = lane >> 2, c4 = lane & 3;
-  const int gw = blockIdx.y * AG + 32 * w;
-  double dr[2][4][2], di[2][4][2];
+  for (int item = blockIdx.x; item < ntiles * nchunk; item += gridDim.x) {
+    const int tile = item / nchunk, chunk = item - tile * nchunk;
+    const ProjTile t = a.tiles[tile];
+    const int nocc = a.nocc[t.k];
+    const double2* phi = a.phi + (size_t)a.off[t.k] * a.nbp;
+    const int gw = chunk * AG + 32 * w;
+    if (gw >= a.nbp) continue;   // per warp: no block-level sync below
+    double dr[2][4][2], di[2][4][2];
 #pragma unroll
-  for (int jb = 0; jb < 2; ++jb)
+    for (int jb = 0; jb < 2; ++jb)
 #pragma unroll
-    for (int gb = 0; gb < 4; ++gb) {
-      dr[jb][gb][0] = dr[jb][gb][1] = 0.0;
-      di[jb][gb][0] = di[jb][gb][1] = 0.0;
-    }
-  if (gw < a.nbp) {
+      for (int gb = 0; gb < 4; ++gb) {
+        dr[jb][gb][0] = dr[jb][gb][1] = 0.0;
+        di[jb][gb][0] = di[jb][gb][1] = 0.0;
+      }
     // batched prefetch of NP m-steps (all of nocc = 32 in one batch)
     constexpr int NP = 8;
     for (int mb = 0; mb < nocc; mb += 4 * NP) {
@@ -251,30 +263,31 @@ __global__ void __launch_bounds__(AW * 32) k_proj_apply(ProjArgs a, const double
           }
       }
     }
-  }
-  // D fragment: row j = r4, g = 2 c4 + {0,1}
+    // D fragment: row j = r4, g = 2 c4 + {0,1}
 #pragma unroll
-  for (int jb = 0; jb < 2; ++jb) {
-    const int r = 8 * jb + r4;
-    if (r >= t.nrows) continue;
-    const int row = a.rows ? a.rows[t.row0 + r] : t.row0 + r;
-    if (active && !active[row % band_mod]) continue;
+    for (int jb = 0; jb < 2; ++jb) {
+      const int r = 8 * jb + r4;
+      if (r >= t.nrows) continue;
+      const int row = a.rows ? a.rows[t.row0 + r] : t.row0 + r;
+      if (active && !active[row % band_mod]) continue;
 #pragma unroll
-    for (int gb = 0; gb < 4; ++gb)
+      for (int gb = 0; gb < 4; ++gb)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int g = gw + 8 * gb + 2 * c4 + h;
-        if (g >= a.nbp) continue;
-        const size_t idx = (size_t)row * a.nbp + g;
-        const double2 x = (ca != 0.0) ? Xin[idx] : make_double2(0.0, 0.0);
-        Y[idx] = make_double2(ca * x.x + cb * dr[jb][gb][h], ca * x.y + cb * di[jb][gb][h]);
-      }
+        for (int h = 0; h < 2; ++h) {
+          const int g = gw + 8 * gb + 2 * c4 + h;
+          if (g >= a.nbp) continue;
+          const size_t idx = (size_t)row * a.nbp + g;
+          const double2 x = (ca != 0.0) ? Xin[idx] : make_double2(0.0, 0.0);
+          Y[idx] = make_double2(ca * x.x + cb * dr[jb][gb][h], ca * x.y + cb * di[jb][gb][h]);
+        }
+    }
   }
 }
 
 int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int>& nocc,
               int nbp, cudaStream_t st, bool async) {
   pl.tiles.clear();
+  pl.max_tiles = 0;
   const int n = (int)row_k.size();
   int i = 0;
   int maxocc = 0;
@@ -286,16 +299,9 @@ int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int
     i = j;
   }
   pl.nrows = n;
-  pl.mtiles = (maxocc + CM - 1) / CM;
+  pl.mtiles = std::max(1, (maxocc + CM - 1) / CM);
   const int ntiles = (int)pl.tiles.size();
-  const int base = std::max(1, ntiles * pl.mtiles);
-  int want = (kSM + base - 1) / base;   // ~one 8-warp CTA per SM
-  const int maxsplit = std::max(1, nbp / (16 * CW));
-  pl.nsplit = std::min(std::max(1, want), maxsplit);
-  int len = (nbp + pl.nsplit - 1) / pl.nsplit;
-  len = ((len + 4 * CW - 1) / (4 * CW)) * (4 * CW);
-  pl.split_len = len;
-  pl.nsplit = (nbp + len - 1) / len;
+  pl.nsplit = std::max(1, std::min(kCoefCtas, nbp / (16 * CW)));   // upper bound
   PWB_TRY(pl.dtiles.ensure(std::max<size_t>(1, pl.tiles.size()) * sizeof(ProjTile)));
   if (!pl.tiles.empty()) {
     if (async) {
@@ -312,30 +318,24 @@ int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int
                           cudaMemcpyHostToDevice));
     }
   }
-  const size_t ntm = (size_t)ntiles * pl.mtiles;
+  const size_t ntm = (size_t)std::max(1, ntiles) * pl.mtiles;
   if (pl.counters.bytes < ntm * sizeof(unsigned) || !pl.counters.ptr) {
-    PWB_TRY(pl.counters.ensure(std::max<size_t>(1, ntm) * sizeof(unsigned)));
-    PWB_CUDA(cudaMemset(pl.counters.ptr, 0, std::max<size_t>(1, ntm) * sizeof(unsigned)));
+    PWB_TRY(pl.counters.ensure(ntm * sizeof(unsigned)));
+    PWB_CUDA(cudaMemset(pl.counters.ptr, 0, ntm * sizeof(unsigned)));
   }
   return PWB_OK;
 }
 
 size_t proj_part_elems(const ProjPlan& pl) {
-  return (size_t)pl.nsplit * plan_tiles(pl) * pl.mtiles * CM * TR;
+  return (size_t)pl.nsplit * std::max(1, plan_tiles(pl)) * pl.mtiles * CM * TR;
 }
 
 int proj_plan_device(ProjPlan& pl, int max_tiles, int maxocc, int nbp) {
   pl.tiles.clear();
   pl.max_tiles = max_tiles;
   pl.nrows = max_tiles * TR;
-  pl.mtiles = (maxocc + CM - 1) / CM;
-  // fixed split so a tile stays spread over the SMs however few tiles are active
-  const int maxsplit = std::max(1, nbp / (16 * CW));
-  pl.nsplit = std::min(maxsplit, std::max(1, kSM / 2));
-  int len = (nbp + pl.nsplit - 1) / pl.nsplit;
-  len = ((len + 4 * CW - 1) / (4 * CW)) * (4 * CW);
-  pl.split_len = len;
-  pl.nsplit = (nbp + len - 1) / len;
+  pl.mtiles = std::max(1, (maxocc + CM - 1) / CM);
+  pl.nsplit = std::max(1, std::min(kCoefCtas, nbp / (16 * CW)));   // upper bound
   PWB_TRY(pl.dtiles.ensure(std::max<size_t>(1, max_tiles) * sizeof(ProjTile)));
   const size_t ntm = (size_t)std::max(1, max_tiles) * pl.mtiles;
   PWB_TRY(pl.counters.ensure(ntm * sizeof(unsigned)));
@@ -345,29 +345,31 @@ int proj_plan_device(ProjPlan& pl, int max_tiles, int maxocc, int nbp) {
 
 int proj_coeffs(const ProjPlan& pl, ProjArgs a, const double2* X, double2* part, double2* C,
                 cudaStream_t st) {
-  const int nt = plan_tiles(pl);
-  if (nt == 0) return PWB_OK;
+  const int cap = plan_tiles(pl);
+  if (cap == 0) return PWB_OK;
   a.tiles = reinterpret_cast<const ProjTile*>(pl.dtiles.ptr);
   a.nrows_total = pl.nrows;
-  dim3 grid((unsigned)nt, pl.mtiles, pl.nsplit);
-  k_proj_coef<<<grid, CW * 32, 0, st>>>(a, X, pl.split_len, pl.nsplit, part, C,
-                                        reinterpret_cast<unsigned*>(pl.counters.ptr));
+  const long items = (long)cap * pl.mtiles * pl.nsplit;
+  const int grid = (int)std::min<long>(items, kCoefCtas);
+  k_proj_coef<<<grid, CW * 32, 0, st>>>(a, X, (int)pl.tiles.size(), cap, pl.mtiles, pl.nsplit,
+                                        part, C, reinterpret_cast<unsigned*>(pl.counters.ptr));
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
 
 int proj_apply(const ProjPlan& pl, ProjArgs a, const double2* C, const double2* Xin, double2* Y,
                double ca, double cb, const int* active, int band_mod, cudaStream_t st) {
-  const int nt = plan_tiles(pl);
-  if (nt == 0) return PWB_OK;
+  const int cap = plan_tiles(pl);
+  if (cap == 0) return PWB_OK;
   a.tiles = reinterpret_cast<const ProjTile*>(pl.dtiles.ptr);
   a.nrows_total = pl.nrows;
-  dim3 grid((unsigned)nt, (a.nbp + AG - 1) / AG);
-  k_proj_apply<<<grid, AW * 32, 0, st>>>(a, C, Xin, Y, ca, cb, active, band_mod > 0 ? band_mod : 1);
+  const long items = (long)cap * ((a.nbp + AG - 1) / AG);
+  const int grid = (int)std::min<long>(items, kApplyCtas);
+  k_proj_apply<<<grid, AW * 32, 0, st>>>(a, C, Xin, Y, ca, cb, active,
+                                         band_mod > 0 ? band_mod : 1, (int)pl.tiles.size());
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
-
 
 // ---------------------------------------------------------------------------
 // Fused Q in ONE launch with a thread-block cluster per row tile:
