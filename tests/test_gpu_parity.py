@@ -183,3 +183,40 @@ def test_kpoint_chi0_matches_gamma_supercell():
     cube = drho.reshape((nx, ny, nz), order="F")
     dup = np.concatenate([cube, cube], axis=0).ravel(order="F")
     assert rel(dup, z["drho_sup"]) < 1e-8
+
+
+def test_two_phase_sharded_chi0_on_one_gpu(metal):
+    """The per-rank C-ABI path (pwb_chi0_begin / pwb_chi0_finish on a band range),
+    run for both halves in one process: the reduced Fermi numerator and the sum of
+    the partial delta rho equal the unsharded chi0 (what NCCL does across GPUs)."""
+    import ctypes
+
+    import torch
+    from paper_2505_02319_b200 import _lib
+    from paper_2505_02319_b200.device import device_state, ptr, shard_range
+    from paper_2505_02319_b200.response import apply_chi0
+    gs = product_gs(metal)
+    tol = np.full(gs.n_occ, 1e-11)
+    full, _ = apply_chi0(gs, metal["dv"][0], tol)
+    ds = device_state(gs)
+    lib = _lib.load()
+    dv = torch.from_numpy(np.ascontiguousarray(metal["dv"][0])).cuda()
+    ranges = [shard_range(ds.nocc, r, 2) for r in range(2)]
+    fs = []
+    for b0, b1 in ranges:
+        f = torch.zeros(2, dtype=torch.float64, device="cuda")
+        _lib.check(lib.pwb_chi0_begin(ds.handle, b0, b1, ptr(dv), ptr(f)))
+        fs.append(f[0].item())
+    total = torch.tensor([sum(fs), 0.0], dtype=torch.float64, device="cuda")
+    parts = []
+    for b0, b1 in ranges:
+        f = torch.zeros(2, dtype=torch.float64, device="cuda")
+        _lib.check(lib.pwb_chi0_begin(ds.handle, b0, b1, ptr(dv), ptr(f)))
+        drho = torch.empty(gs.grids.n_g, dtype=torch.float64, device="cuda")
+        its = np.zeros(b1 - b0, dtype=np.int32)
+        tl = np.ascontiguousarray(tol[b0:b1])
+        _lib.check(lib.pwb_chi0_finish(ds.handle, ptr(total), ctypes.c_void_p(tl.ctypes.data),
+                                       ptr(drho), ctypes.c_void_p(its.ctypes.data)))
+        parts.append(drho.cpu().numpy())
+    assert abs(sum(fs)) > 0     # metallic: the Fermi-level term is exercised
+    assert rel(parts[0] + parts[1], full) < 1e-12
