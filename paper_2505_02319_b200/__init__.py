@@ -17,3 +17,14 @@ __version__ = "0.1.0"
 
 from .errors import (ArchiveError, ConfigurationError, InvariantViolationError,  # noqa: F401
                      NonConvergenceError, PwdysonError)
+
+
+def install(package="pwdyson"):
+    """Route the reference package's chi0 path through libpwb200 (see dropin.py)."""
+    from .dropin import install as _install
+    return _install(package)
+
+
+def uninstall(package="pwdyson"):
+    from .dropin import uninstall as _uninstall
+    return _uninstall(package)

@@ -56,6 +56,7 @@ SIGNATURES = {
     "pwb_row_norm_rows": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int, _c_dbl_p]),
     "pwb_chi0_parts": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "pwb_project_generic": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]),
+    "pwb_project_host": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]),
     "pwb_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "pwb_profile_reset": (ctypes.c_int, []),
     "pwb_profile_read": (ctypes.c_int, [_vp, _vp, _vp]),

@@ -421,6 +421,20 @@ int pwb_project_generic(int nb, int nocc, const double* phi, int ncol, double* x
   return PWB_OK;
 }
 
+int pwb_project_host(int nb, int nocc, const double* phi_host, int ncol, double* x_host) {
+  if (nb < 1 || nocc < 1 || ncol < 0) return fail(PWB_ERR_VALUE, "bad projector sizes");
+  if (ncol == 0) return PWB_OK;
+  DevBuf dphi, dx;
+  const size_t bp = (size_t)nocc * nb * sizeof(double2), bx = (size_t)ncol * nb * sizeof(double2);
+  PWB_TRY(dphi.ensure(bp));
+  PWB_TRY(dx.ensure(bx));
+  PWB_CUDA(cudaMemcpy(dphi.ptr, phi_host, bp, cudaMemcpyHostToDevice));
+  PWB_CUDA(cudaMemcpy(dx.ptr, x_host, bx, cudaMemcpyHostToDevice));
+  PWB_TRY(pwb_project_generic(nb, nocc, as<double>(dphi), ncol, as<double>(dx)));
+  PWB_CUDA(cudaMemcpy(x_host, dx.ptr, bx, cudaMemcpyDeviceToHost));
+  return PWB_OK;
+}
+
 // Pieces of chi0 for a perturbation dv (all bands): diag_host[2*b + {0,1}] =
 // <phi_b, dv phi_b> (complex, response.py:53-55) and, if dphi is non-NULL,
 // the occupied-subspace response Phi (W o M) as device rows (response.py:101-107).
