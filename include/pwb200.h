@@ -158,7 +158,8 @@ int pwb_row_norm_rows(pwb_grid* grid, int nrows, const int* band_k, const double
 int pwb_chi0_parts(pwb_state* st, const double* dv, double* diag_host, double* dphi);
 
 /* project_out_occupied (sternheimer.py:28-30) for an arbitrary block: phi =
- * nocc device rows of length nb (orthonormal), x = ncol device rows, in place. */
+ * nocc device rows of length nb (orthonormal), x = ncol device rows, in place.
+ * Asynchronous on the legacy default stream.                                  */
 int pwb_project_generic(int nb, int nocc, const double* phi, int ncol, double* x);
 /* same with host buffers (phi: nocc rows of nb complex, x: ncol rows, in place) */
 int pwb_project_host(int nb, int nocc, const double* phi_host, int ncol, double* x_host);

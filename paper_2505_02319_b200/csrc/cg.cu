@@ -295,13 +295,8 @@ int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* activ
   a.rows = rows;
   a.ntiles = ntiles;
   cudaEvent_t e = prof().begin(s);
-  static const bool fused = getenv("PWB_PROJ_FUSED") != nullptr;   // cluster variant (slower
-  if (fused) {                                                      // at cfg1 sizes, kept)
-    PWB_TRY(proj_q(pl, a, X, X, 1.0, -1.0, active, band_mod, s));
-  } else {
-    PWB_TRY(proj_coeffs(pl, a, X, part, cmat, s));
-    PWB_TRY(proj_apply(pl, a, cmat, X, X, 1.0, -1.0, active, band_mod, s));
-  }
+  PWB_TRY(proj_coeffs(pl, a, X, part, cmat, s));
+  PWB_TRY(proj_apply(pl, a, cmat, X, X, 1.0, -1.0, active, band_mod, s));
   prof().end(PROF_Q, e, s, pl.nrows);
   return PWB_OK;
 }

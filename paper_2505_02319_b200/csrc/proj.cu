@@ -3,20 +3,26 @@
 // sternheimer.py:28-30 and response.py:129,138.
 //
 //   coef :  C[row][m] = sum_g conj(Phi_k[m][g]) X[row][g]
-//           split-K over the sphere; warps of a CTA reduce in smem, splits are
-//           reduced in FIXED split order by the last CTA to finish a tile
+//           split-K over the sphere; the warps of a CTA reduce in smem, splits
+//           are reduced in FIXED split order by the last CTA to finish a tile
 //           (threadfence + arrival counter): bitwise reproducible, one launch.
 //   apply:  Y[row][g] = a X[row][g] + b sum_m Phi_k[m][g] C[row][m]
 //
-// Both kernels are persistent over a work-item list ((tile, m block, split)
-// and (tile, g chunk)) with the grid sized to the SMs, and the number of
-// splits is chosen on the device from the live tile count: with active-row
-// compaction the tile count shrinks every CG iteration, and a fixed grid of
-// mostly-exiting CTAs (or too few splits) was measured to dominate the tail.
+// Data movement: both kernels are persistent (one CTA per SM) and stream
+// their operands through a ring of shared-memory stages filled by TMA bulk
+// copies (cp.async.bulk -> UBLKCP, one 1 KB copy per row chunk, completion
+// on an mbarrier with expect_tx).  A dedicated producer warp keeps SC
+// stages in flight (full/empty mbarrier ring); rows of X are gathered through the
+// compacted row list, so active-row compaction costs nothing here.  The
+// smem row strides are padded so that the DMMA fragment loads (8 rows x
+// 4 consecutive complex) are bank-conflict free.
 //
-// Complex products are four real DMMAs (re.re, im.im, re.im, im.re).  Rows of
-// X are grouped in tiles of <= 16 rows sharing one k block; with active-row
-// compaction the tile rows index X through a row list.
+// Padding work is bounded at fragment granularity: a tile of <= 16 rows uses
+// ceil(rows/8) n-fragments, an m block of <= 40 orbitals ceil(m/8)
+// m-fragments (warp-uniform predicates), so ragged N_occ per k (31..35 at
+// BASELINE configs[1]) does not pay for 64-wide blocks.
+//
+// Complex products are four real DMMAs (re.re, im.im, re.im, im.re).
 // Measured on B200: DMMA 37.1 TFLOP/s, DFMA 34.0 TFLOP/s (tools/fp64_peak.cu).
 #include <cstring>
 
@@ -24,13 +30,21 @@
 
 namespace pwb {
 
-constexpr int TR = kProjTileRows;   // rows per tile (2 DMMA n-fragments)
-constexpr int CM = 32;   // m per coef block (4 DMMA m-fragments)
-constexpr int CW = 8;    // warps per coef CTA
-constexpr int AW = 8;    // warps per apply CTA
-constexpr int AG = AW * 32;  // g per apply work item (32 per warp)
-constexpr int kCoefCtas = 2 * kSM;
-constexpr int kApplyCtas = 2 * kSM;
+constexpr int TR = kProjTileRows;   // rows per tile (<= 2 DMMA n-fragments)
+constexpr int KC = 64;              // sphere coefficients per pipeline chunk
+constexpr int MF = 5;               // m fragments per block
+constexpr int CM = 8 * MF;          // orbitals per block
+constexpr int NW = 8;               // warps per CTA
+constexpr int SC = 3;               // pipeline stages
+constexpr int RSC = KC + 4;         // coef smem row stride (double2): 64 B mod 128 B
+constexpr int RSP = KC + 2;         // apply Phi row stride: 32 B mod 128 B
+constexpr int RSX = KC + 4;         // apply X row stride
+constexpr int RSM = CM + 4;         // apply C row stride (44 = 4 mod 8)
+constexpr int kCoefStage = (TR + CM) * RSC;              // double2 per coef stage
+constexpr int kApplyStage = CM * RSP + TR * RSX + TR * RSM;
+constexpr size_t kCoefSmem = (size_t)SC * kCoefStage * 16 + (size_t)(NW / 2) * CM * TR * 16 + 64;
+constexpr size_t kApplySmem = (size_t)SC * kApplyStage * 16 + 64;
+static_assert(kCoefSmem <= 232448 && kApplySmem <= 232448, "stage ring exceeds 227 KB");
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -38,254 +52,495 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-// live split count for `units` (tile x m block) work units
-__device__ __forceinline__ int live_nsplit(int units, int nsplit_max) {
-  int s = (kCoefCtas + units - 1) / max(units, 1);
-  return max(1, min(s, nsplit_max));
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE_%=;\n"
+      " bra WAIT_%=;\n"
+      "DONE_%=:\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(b))
+      : "memory");
+}
+__device__ __forceinline__ int xrow(const ProjArgs& a, const ProjTile& t, int r) {
+  return a.rows ? a.rows[t.row0 + r] : t.row0 + r;
 }
 
-__global__ void __launch_bounds__(CW * 32) k_proj_coef(ProjArgs a, const double2* __restrict__ X,
-                                                       int nt_host, int tile_cap, int mtiles,
-                                                       int nsplit_max, double2* __restrict__ part,
-                                                       double2* __restrict__ C,
-                                                       unsigned* __restrict__ counters) {
-  __shared__ double2 red[CW / 2][CM][TR];
-  __shared__ bool last;
-  const int ntiles = a.ntiles ? *a.ntiles : nt_host;
-  const int units = ntiles * mtiles;
-  const int nsplit = live_nsplit(units, nsplit_max);
-  int split_len = (a.nbp + nsplit - 1) / nsplit;
-  split_len = ((split_len + 4 * CW - 1) / (4 * CW)) * (4 * CW);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r4 = lane >> 2, c4 = lane & 3;
-  const size_t stride = (size_t)tile_cap * mtiles * (CM * TR);   // per split
-  for (int item = blockIdx.x; item < units * nsplit; item += gridDim.x) {
-    const int split = item % nsplit;
-    const int unit = item / nsplit;
-    const int mblk = unit % mtiles, tile = unit / mtiles;
-    const ProjTile t = a.tiles[tile];
-    const int m0 = mblk * CM;
-    const int nocc = a.nocc[t.k];
-    if (m0 >= nocc) continue;   // uniform over the CTA
-    const int g0 = split * split_len;
-    const int g1 = min(a.nbp, g0 + split_len);
-    const double2* phi = a.phi + (size_t)a.off[t.k] * a.nbp;
-    const double2* prow[4];
-    bool pok[4];
+// ---------------------------------------------------------------------------
+// coef: work item = (tile, m block, split); a split is a run of KC chunks.
+struct CoefGeom {
+  int ntiles, mtiles, nsplit, split_chunks, nchunk, nitems;
+};
+
+// The split count is chosen on the device from the live tile count (it shrinks
+// every CG iteration under compaction): the s minimising the modelled time of
+// the busiest CTA, in units of 1/16 chunk: items * (chunks + 1 for the item's
+// smem/partial reduction) * 16 + s for the last CTA's s-way partial sum.
+// (Splitting into single-chunk items looks balanced but measured 6x slower at
+// full rows: the per-item reduction dominates.)  Evaluated warp-parallel
+// (lane l tries s = l + 1, l + 33, ...) by every warp.
+__device__ __forceinline__ CoefGeom coef_geom(const ProjArgs& a, int nt_host, int mtiles,
+                                              int smax) {
+  CoefGeom g;
+  g.ntiles = a.ntiles ? *a.ntiles : nt_host;
+  g.mtiles = mtiles;
+  g.nchunk = a.nbp / KC;
+  const int units = max(1, g.ntiles * mtiles);
+  const int lane = threadIdx.x & 31, grid = gridDim.x;
+  smax = min(smax, g.nchunk);
+  unsigned long long best = ~0ull;
+  for (int s = lane + 1; s <= smax; s += 32) {
+    const int sc = (g.nchunk + s - 1) / s;
+    if ((g.nchunk + sc - 1) / sc != s) continue;   // only exact split counts
+    const unsigned long long busiest =
+        (unsigned long long)((units * s + grid - 1) / grid) * (sc + 1) * 16 + s;
+    best = min(best, (busiest << 16) | (unsigned)s);   // ties -> fewer splits
+  }
 #pragma unroll
-    for (int ma = 0; ma < 4; ++ma) {
-      const int m = m0 + 8 * ma + r4;
-      pok[ma] = m < nocc;
-      prow[ma] = phi + (size_t)(pok[ma] ? m : 0) * a.nbp;
-    }
-    const double2* xrw[2];
-    bool xok[2];
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      const int r = 8 * nb + r4;
-      xok[nb] = r < t.nrows;
-      xrw[nb] = X + (size_t)(xok[nb] ? (a.rows ? a.rows[t.row0 + r] : t.row0 + r) : 0) * a.nbp;
-    }
-    double cr[4][2][2], ci[4][2][2];
-#pragma unroll
-    for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
-        cr[ma][nb][0] = cr[ma][nb][1] = 0.0;
-        ci[ma][nb][0] = ci[ma][nb][1] = 0.0;
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  const int s = (int)(best & 0xffff);
+  g.split_chunks = (g.nchunk + s - 1) / s;
+  g.nsplit = s;
+  g.nitems = g.ntiles * mtiles * g.nsplit;
+  return g;
+}
+
+struct CoefItem {
+  ProjTile t;
+  int tile, mblk, m0, nm, c0, c1;   // nm orbitals from m0; chunks [c0, c1)
+};
+
+__device__ __forceinline__ bool coef_item(const ProjArgs& a, const CoefGeom& g, int item,
+                                          CoefItem& it) {
+  const int split = item % g.nsplit;
+  const int unit = item / g.nsplit;
+  it.mblk = unit % g.mtiles;
+  it.tile = unit / g.mtiles;
+  it.t = a.tiles[it.tile];
+  it.m0 = it.mblk * CM;
+  it.nm = min(CM, a.nocc[it.t.k] - it.m0);
+  it.c0 = split * g.split_chunks;
+  it.c1 = min(g.nchunk, it.c0 + g.split_chunks);
+  return it.nm > 0 && it.c0 < it.c1 && it.t.nrows > 0;
+}
+
+// walks the (item, chunk) sequence of this CTA, skipping empty items
+struct CoefCursor {
+  int item, chunk;
+  CoefItem it;
+  bool valid;
+  __device__ void first(const ProjArgs& a, const CoefGeom& g) {
+    item = blockIdx.x;
+    valid = false;
+    for (; item < g.nitems; item += gridDim.x)
+      if (coef_item(a, g, item, it)) {
+        valid = true;
+        chunk = it.c0;
+        return;
       }
-    // batched prefetch: the fragments of NP k-steps are loaded before any is used
-    constexpr int NP = 4;
-    for (int gb = g0 + 4 * w; gb < g1; gb += 4 * CW * NP) {
-      double2 av[NP][4], bv[NP][2];
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-        const int gg = gb + 4 * CW * u + c4;
-        const bool gok = gg < g1;
-#pragma unroll
-        for (int ma = 0; ma < 4; ++ma)
-          av[u][ma] = (gok && pok[ma]) ? __ldg(&prow[ma][gg]) : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-          bv[u][nb] = (gok && xok[nb]) ? xrw[nb][gg] : make_double2(0.0, 0.0);
+  }
+  __device__ void next(const ProjArgs& a, const CoefGeom& g) {
+    if (++chunk < it.c1) return;
+    valid = false;
+    for (item += gridDim.x; item < g.nitems; item += gridDim.x)
+      if (coef_item(a, g, item, it)) {
+        valid = true;
+        chunk = it.c0;
+        return;
       }
-      // conj(phi) * x : re = pr xr + pi xi ; im = pr xi - pi xr (part-major issue)
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-#pragma unroll
-        for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-          for (int nb = 0; nb < 2; ++nb) {
-            dmma(cr[ma][nb][0], cr[ma][nb][1], av[u][ma].x, bv[u][nb].x);
-            dmma(ci[ma][nb][0], ci[ma][nb][1], av[u][ma].x, bv[u][nb].y);
-          }
-#pragma unroll
-        for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-          for (int nb = 0; nb < 2; ++nb) {
-            dmma(cr[ma][nb][0], cr[ma][nb][1], av[u][ma].y, bv[u][nb].y);
-            dmma(ci[ma][nb][0], ci[ma][nb][1], -av[u][ma].y, bv[u][nb].x);
-          }
-      }
+  }
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+// barrier among the NW consumer warps only (the producer warp runs free)
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NW * 32) : "memory");
+}
+
+// Producer warp (warp NW) of the coef kernel: walks the same (item, chunk)
+// sequence as the consumers and keeps SC stages in flight; lane l copies X
+// row l and Phi rows l and l + 32 of the current item (sources resolved once
+// per item, so the row-list lookups are off the per-chunk path).
+__device__ void coef_producer(const ProjArgs& a, const CoefGeom& g, const double2* X,
+                              double2* stages, uint64_t* full, uint64_t* empty, int lane) {
+  CoefCursor c;
+  c.first(a, g);
+  int cur = -1;
+  const double2 *xs = nullptr, *p0 = nullptr, *p1 = nullptr;
+  uint32_t bytes = 0;
+  for (unsigned n = 0; c.valid; ++n) {
+    const int s = n % SC;
+    if (n >= SC) mbar_wait(&empty[s], ((n / SC) + 1) & 1);
+    if (c.item != cur) {
+      cur = c.item;
+      const double2* phi = a.phi + ((size_t)a.off[c.it.t.k] + c.it.m0) * a.nbp;
+      xs = lane < c.it.t.nrows ? X + (size_t)xrow(a, c.it.t, lane) * a.nbp : nullptr;
+      p0 = lane < c.it.nm ? phi + (size_t)lane * a.nbp : nullptr;
+      p1 = lane + 32 < c.it.nm ? phi + (size_t)(lane + 32) * a.nbp : nullptr;
+      bytes = (uint32_t)(c.it.t.nrows + c.it.nm) * KC * 16;
     }
-    // fixed-order warp reduction in two halves: warp w (< CW/2) adds w + CW/2
-    if (w >= CW / 2) {
-#pragma unroll
-      for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            red[w - CW / 2][8 * ma + r4][8 * nb + 2 * c4 + h] =
-                make_double2(cr[ma][nb][h], ci[ma][nb][h]);
-    }
-    __syncthreads();
-    if (w < CW / 2) {
-#pragma unroll
-      for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            double2& slot = red[w][8 * ma + r4][8 * nb + 2 * c4 + h];
-            slot = make_double2(cr[ma][nb][h] + slot.x, ci[ma][nb][h] + slot.y);
-          }
-    }
-    __syncthreads();
-    const size_t tile_id = (size_t)tile * mtiles + mblk;
-    double2* mypart = part + (size_t)split * stride + tile_id * (CM * TR);
-    for (int i = threadIdx.x; i < CM * TR; i += CW * 32) {
-      const int m = i / TR, r = i - m * TR;
-      double2 s = red[0][m][r];
-#pragma unroll
-      for (int q = 1; q < CW / 2; ++q) s = cadd(s, red[q][m][r]);
-      if (nsplit == 1) {
-        if (r < t.nrows && m0 + m < nocc) C[(size_t)(t.row0 + r) * a.ldc + m0 + m] = s;
-      } else {
-        mypart[i] = s;
-      }
-    }
-    if (nsplit > 1) {
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(&counters[tile_id], 1u);
-        last = (prev == (unsigned)nsplit - 1);
-      }
-      __syncthreads();
-      if (last) {
-        __threadfence();
-        const double2* p0 = part + tile_id * (CM * TR);
-        for (int i = threadIdx.x; i < CM * TR; i += CW * 32) {
-          const int m = i / TR, r = i - m * TR;
-          double2 s = __ldcg(&p0[i]);
-          int q = 1;
-          // loads issued 8 at a time (serialised on L2 latency otherwise), summed in order
-          for (; q + 8 <= nsplit; q += 8) {
-            double2 v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __ldcg(&p0[(size_t)(q + u) * stride + i]);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) s = cadd(s, v[u]);
-          }
-          for (; q < nsplit; ++q) s = cadd(s, __ldcg(&p0[(size_t)q * stride + i]));
-          if (r < t.nrows && m0 + m < nocc) C[(size_t)(t.row0 + r) * a.ldc + m0 + m] = s;
-        }
-        if (threadIdx.x == 0) counters[tile_id] = 0u;
-      }
-    }
-    __syncthreads();   // red / last reused by the next item
+    const size_t g0 = (size_t)c.chunk * KC;
+    double2* buf = stages + s * kCoefStage;
+    if (lane == 0) mbar_expect_tx(&full[s], bytes);
+    __syncwarp();
+    if (xs) bulk_g2s(buf + lane * RSC, xs + g0, KC * 16, &full[s]);
+    if (p0) bulk_g2s(buf + (TR + lane) * RSC, p0 + g0, KC * 16, &full[s]);
+    if (p1) bulk_g2s(buf + (TR + lane + 32) * RSC, p1 + g0, KC * 16, &full[s]);
+    c.next(a, g);
   }
 }
 
-// work item = (tile, chunk of AG g); warp w covers g0 + 32 w .. + 32
-__global__ void __launch_bounds__(AW * 32) k_proj_apply(ProjArgs a, const double2* __restrict__ C,
-                                                        const double2* __restrict__ Xin,
-                                                        double2* __restrict__ Y, double ca,
-                                                        double cb, const int* __restrict__ active,
-                                                        int band_mod, int nt_host) {
-  const int ntiles = a.ntiles ? *a.ntiles : nt_host;
-  const int nchunk = (a.nbp + AG - 1) / AG;
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    k_proj_coef(ProjArgs a, const double2* __restrict__ X, int nt_host, int tile_cap, int mtiles,
+                int smax, double2* __restrict__ part, double2* __restrict__ C,
+                unsigned* __restrict__ counters) {
+  extern __shared__ __align__(128) double2 sm[];
+  double2* stages = sm;
+  double2* red = sm + SC * kCoefStage;   // [NW/2][CM][TR]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + (NW / 2) * CM * TR);
+  uint64_t* empty = full + SC;
+  __shared__ bool last;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r4 = lane >> 2, c4 = lane & 3;
-  for (int item = blockIdx.x; item < ntiles * nchunk; item += gridDim.x) {
-    const int tile = item / nchunk, chunk = item - tile * nchunk;
-    const ProjTile t = a.tiles[tile];
-    const int nocc = a.nocc[t.k];
-    const double2* phi = a.phi + (size_t)a.off[t.k] * a.nbp;
-    const int gw = chunk * AG + 32 * w;
-    if (gw >= a.nbp) continue;   // per warp: no block-level sync below
-    double dr[2][4][2], di[2][4][2];
+  const CoefGeom g = coef_geom(a, nt_host, mtiles, smax);
+  const size_t stride = (size_t)tile_cap * mtiles * (CM * TR);   // partials per split
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SC; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (w == NW) {
+    coef_producer(a, g, X, stages, full, empty, lane);
+    return;
+  }
+  CoefCursor cons;
+  cons.first(a, g);
+  double cr[MF][2][2], ci[MF][2][2];
+  unsigned seq = 0;
+  while (cons.valid) {
+    const CoefItem& it = cons.it;
+    if (cons.chunk == it.c0) {
 #pragma unroll
-    for (int jb = 0; jb < 2; ++jb)
+      for (int ma = 0; ma < MF; ++ma)
 #pragma unroll
-      for (int gb = 0; gb < 4; ++gb) {
-        dr[jb][gb][0] = dr[jb][gb][1] = 0.0;
-        di[jb][gb][0] = di[jb][gb][1] = 0.0;
-      }
-    // batched prefetch of NP m-steps (all of nocc = 32 in one batch)
-    constexpr int NP = 8;
-    for (int mb = 0; mb < nocc; mb += 4 * NP) {
-      double2 av[NP][2], bv[NP][4];
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-        const int mm = mb + 4 * u + c4;
-        const bool mok = mm < nocc;
-#pragma unroll
-        for (int jb = 0; jb < 2; ++jb) {
-          const int r = 8 * jb + r4;   // A[j = r4][k = c4] = C[row j][m + c4]
-          av[u][jb] = (mok && r < t.nrows) ? C[(size_t)(t.row0 + r) * a.ldc + mm]
-                                           : make_double2(0.0, 0.0);
+        for (int nb = 0; nb < 2; ++nb) {
+          cr[ma][nb][0] = cr[ma][nb][1] = 0.0;
+          ci[ma][nb][0] = ci[ma][nb][1] = 0.0;
         }
+    }
+    const int s = seq % SC;
+    mbar_wait(&full[s], (seq / SC) & 1);
+    const double2* xs = stages + s * kCoefStage;
+    const double2* ps = xs + TR * RSC;
+    const int nfm = (it.nm + 7) >> 3, nfn = (it.t.nrows + 7) >> 3;
 #pragma unroll
-        for (int gb = 0; gb < 4; ++gb) {
-          const int g = gw + 8 * gb + r4;   // B[k = c4][n = r4] = Phi[m + c4][g]
-          bv[u][gb] = (mok && g < a.nbp) ? __ldg(&phi[(size_t)mm * a.nbp + g])
-                                         : make_double2(0.0, 0.0);
+    for (int kk = 0; kk < KC / (4 * NW); ++kk) {
+      const int gl = 4 * (w + NW * kk) + c4;
+      double2 av[MF], bv[2];
+#pragma unroll
+      for (int ma = 0; ma < MF; ++ma)
+        av[ma] = ma < nfm ? ps[(8 * ma + r4) * RSC + gl] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+        bv[nb] = nb < nfn ? xs[(8 * nb + r4) * RSC + gl] : make_double2(0.0, 0.0);
+      // conj(phi) * x : re = pr xr + pi xi ; im = pr xi - pi xr
+#pragma unroll
+      for (int ma = 0; ma < MF; ++ma) {
+        if (ma >= nfm) break;
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+          if (nb >= nfn) break;
+          dmma(cr[ma][nb][0], cr[ma][nb][1], av[ma].x, bv[nb].x);
+          dmma(ci[ma][nb][0], ci[ma][nb][1], av[ma].x, bv[nb].y);
         }
       }
-      // C * Phi : re = cr pr - ci pi ; im = cr pi + ci pr (part-major issue order)
 #pragma unroll
-      for (int u = 0; u < NP; ++u) {
+      for (int ma = 0; ma < MF; ++ma) {
+        if (ma >= nfm) break;
 #pragma unroll
-        for (int jb = 0; jb < 2; ++jb)
-#pragma unroll
-          for (int gb = 0; gb < 4; ++gb) {
-            dmma(dr[jb][gb][0], dr[jb][gb][1], av[u][jb].x, bv[u][gb].x);
-            dmma(di[jb][gb][0], di[jb][gb][1], av[u][jb].x, bv[u][gb].y);
-          }
-#pragma unroll
-        for (int jb = 0; jb < 2; ++jb)
-#pragma unroll
-          for (int gb = 0; gb < 4; ++gb) {
-            dmma(dr[jb][gb][0], dr[jb][gb][1], -av[u][jb].y, bv[u][gb].y);
-            dmma(di[jb][gb][0], di[jb][gb][1], av[u][jb].y, bv[u][gb].x);
-          }
+        for (int nb = 0; nb < 2; ++nb) {
+          if (nb >= nfn) break;
+          dmma(cr[ma][nb][0], cr[ma][nb][1], av[ma].y, bv[nb].y);
+          dmma(ci[ma][nb][0], ci[ma][nb][1], -av[ma].y, bv[nb].x);
+        }
       }
     }
-    // D fragment: row j = r4, g = 2 c4 + {0,1}
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
+    ++seq;
+    if (cons.chunk + 1 >= it.c1) {
+      const CoefItem done = it;
+      // fixed-order warp reduction in two halves: warp w (< NW/2) adds w + NW/2
+      if (w >= NW / 2) {
 #pragma unroll
-    for (int jb = 0; jb < 2; ++jb) {
-      const int r = 8 * jb + r4;
-      if (r >= t.nrows) continue;
-      const int row = a.rows ? a.rows[t.row0 + r] : t.row0 + r;
-      if (active && !active[row % band_mod]) continue;
+        for (int ma = 0; ma < MF; ++ma)
 #pragma unroll
-      for (int gb = 0; gb < 4; ++gb)
+          for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              red[((w - NW / 2) * CM + 8 * ma + r4) * TR + 8 * nb + 2 * c4 + h] =
+                  make_double2(cr[ma][nb][h], ci[ma][nb][h]);
+      }
+      consumer_sync();
+      if (w < NW / 2) {
+#pragma unroll
+        for (int ma = 0; ma < MF; ++ma)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              double2& slot = red[(w * CM + 8 * ma + r4) * TR + 8 * nb + 2 * c4 + h];
+              slot = make_double2(cr[ma][nb][h] + slot.x, ci[ma][nb][h] + slot.y);
+            }
+      }
+      consumer_sync();
+      const size_t tile_id = (size_t)done.tile * mtiles + done.mblk;
+      const int split = done.c0 / g.split_chunks;
+      double2* mypart = part + (size_t)split * stride + tile_id * (CM * TR);
+      for (int i = threadIdx.x; i < CM * TR; i += NW * 32) {
+        const int m = i / TR, r = i - m * TR;
+        double2 v = red[i];
+#pragma unroll
+        for (int q = 1; q < NW / 2; ++q) v = cadd(v, red[q * CM * TR + i]);
+        if (g.nsplit == 1) {
+          if (r < done.t.nrows && m < done.nm)
+            C[(size_t)(done.t.row0 + r) * a.ldc + done.m0 + m] = v;
+        } else {
+          mypart[i] = v;
+        }
+      }
+      if (g.nsplit > 1) {
+        __threadfence();
+        consumer_sync();
+        if (threadIdx.x == 0) {
+          const unsigned prev = atomicAdd(&counters[tile_id], 1u);
+          last = (prev == (unsigned)g.nsplit - 1);
+        }
+        consumer_sync();
+        if (last) {
+          __threadfence();
+          const double2* p0 = part + tile_id * (CM * TR);
+          for (int i = threadIdx.x; i < CM * TR; i += NW * 32) {
+            const int m = i / TR, r = i - m * TR;
+            if (r >= done.t.nrows || m >= done.nm) continue;
+            double2 v = __ldcg(&p0[i]);
+            int q = 1;
+            // loads issued 8 at a time (serialised on L2 latency otherwise), summed in order
+            for (; q + 8 <= g.nsplit; q += 8) {
+              double2 u[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) u[j] = __ldcg(&p0[(size_t)(q + j) * stride + i]);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v = cadd(v, u[j]);
+            }
+            for (; q < g.nsplit; ++q) v = cadd(v, __ldcg(&p0[(size_t)q * stride + i]));
+            C[(size_t)(done.t.row0 + r) * a.ldc + done.m0 + m] = v;
+          }
+          if (threadIdx.x == 0) counters[tile_id] = 0u;
+        }
+      }
+      consumer_sync();   // red / last reused by the next item
+    }
+    cons.next(a, g);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// apply: work item = (tile, KC chunk of g); one stage per m block of the item
+// (C block + Phi block, plus the X chunk with the last m block).  Consumer
+// warp w owns the 8 g of fragment w for both row fragments.
+struct ApplyCursor {
+  int item, mblk, nitems, nchunk, nmb;
+  ProjTile t;
+  int nocc;
+  bool valid;
+  __device__ void load(const ProjArgs& a) {
+    const int tile = item / nchunk;
+    t = a.tiles[tile];
+    nocc = a.nocc[t.k];
+    nmb = (nocc + CM - 1) / CM;
+  }
+  __device__ void first(const ProjArgs& a, int ntiles) {
+    nchunk = a.nbp / KC;
+    nitems = ntiles * nchunk;
+    item = blockIdx.x;
+    mblk = 0;
+    valid = item < nitems;
+    if (valid) load(a);
+  }
+  __device__ void next(const ProjArgs& a) {
+    if (++mblk < nmb) return;
+    mblk = 0;
+    item += gridDim.x;
+    valid = item < nitems;
+    if (valid) load(a);
+  }
+};
+
+// Producer warp of the apply kernel: lane l copies Phi rows l, l + 32 of the
+// m block, and (l < 16) X row l of the chunk, (16 <= l < 32) C row l - 16.
+__device__ void apply_producer(const ProjArgs& a, const double2* C, const double2* Xin,
+                               bool want_x, int ntiles, double2* stages, uint64_t* full,
+                               uint64_t* empty, int lane) {
+  ApplyCursor c;
+  c.first(a, ntiles);
+  for (unsigned n = 0; c.valid; ++n) {
+    const int s = n % SC;
+    if (n >= SC) mbar_wait(&empty[s], ((n / SC) + 1) & 1);
+    const int nr = c.t.nrows;
+    const int m0 = c.mblk * CM, nm = min(CM, c.nocc - m0);
+    const bool with_x = want_x && c.mblk == c.nmb - 1;
+    const size_t g0 = (size_t)(c.item % c.nchunk) * KC;
+    const uint32_t bytes = (uint32_t)nm * KC * 16 + (with_x ? (uint32_t)nr * KC * 16 : 0u) +
+                           (uint32_t)nr * nm * 16;
+    double2* ps = stages + s * kApplyStage;
+    double2* xs = ps + CM * RSP;
+    double2* cs = xs + TR * RSX;
+    if (lane == 0) mbar_expect_tx(&full[s], bytes);
+    __syncwarp();
+    const double2* phi = a.phi + ((size_t)a.off[c.t.k] + m0) * a.nbp + g0;
+    if (lane < nm) bulk_g2s(ps + lane * RSP, phi + (size_t)lane * a.nbp, KC * 16, &full[s]);
+    if (lane + 32 < nm)
+      bulk_g2s(ps + (lane + 32) * RSP, phi + (size_t)(lane + 32) * a.nbp, KC * 16, &full[s]);
+    if (lane < TR) {
+      if (with_x && lane < nr)
+        bulk_g2s(xs + lane * RSX, Xin + (size_t)xrow(a, c.t, lane) * a.nbp + g0, KC * 16,
+                 &full[s]);
+    } else if (lane - TR < nr) {
+      const int r = lane - TR;
+      bulk_g2s(cs + r * RSM, C + (size_t)(c.t.row0 + r) * a.ldc + m0, nm * 16, &full[s]);
+    }
+    c.next(a);
+  }
+}
+
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    k_proj_apply(ProjArgs a, const double2* __restrict__ C, const double2* __restrict__ Xin,
+                 double2* __restrict__ Y, double ca, double cb, const int* __restrict__ active,
+                 int band_mod, int nt_host) {
+  extern __shared__ __align__(128) double2 sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + SC * kApplyStage);
+  uint64_t* empty = full + SC;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r4 = lane >> 2, c4 = lane & 3;
+  const int ntiles = a.ntiles ? *a.ntiles : nt_host;
+  const bool want_x = ca != 0.0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SC; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (w == NW) {
+    apply_producer(a, C, Xin, want_x, ntiles, sm, full, empty, lane);
+    return;
+  }
+  ApplyCursor cons;
+  cons.first(a, ntiles);
+  double dr[2][2], di[2][2];
+  unsigned seq = 0;
+  while (cons.valid) {
+    if (cons.mblk == 0) {
+      dr[0][0] = dr[0][1] = dr[1][0] = dr[1][1] = 0.0;
+      di[0][0] = di[0][1] = di[1][0] = di[1][1] = 0.0;
+    }
+    const int s = seq % SC;
+    mbar_wait(&full[s], (seq / SC) & 1);
+    const double2* ps = sm + s * kApplyStage;
+    const double2* xs = ps + CM * RSP;
+    const double2* cs = xs + TR * RSX;
+    const int nm = min(CM, cons.nocc - cons.mblk * CM);
+    const int nfn = (cons.t.nrows + 7) >> 3;
+    for (int ms = 0; ms < nm; ms += 4) {
+      const int m = ms + c4;
+      const bool mok = m < nm;   // contraction index: padding must be exactly zero
+      double2 av[2];
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb)   // A[j = r4][k = c4] = C[row j][m]
+        av[jb] = (mok && jb < nfn) ? cs[(8 * jb + r4) * RSM + m] : make_double2(0.0, 0.0);
+      const double2 bv = mok ? ps[m * RSP + 8 * w + r4] : make_double2(0.0, 0.0);   // Phi[m][g]
+      // C * Phi : re = cr pr - ci pi ; im = cr pi + ci pr
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb) {
+        if (jb >= nfn) break;
+        dmma(dr[jb][0], dr[jb][1], av[jb].x, bv.x);
+        dmma(di[jb][0], di[jb][1], av[jb].x, bv.y);
+      }
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb) {
+        if (jb >= nfn) break;
+        dmma(dr[jb][0], dr[jb][1], -av[jb].y, bv.y);
+        dmma(di[jb][0], di[jb][1], av[jb].y, bv.x);
+      }
+    }
+    if (cons.mblk == cons.nmb - 1) {   // epilogue: D fragment row j = r4, g = 2 c4 + {0,1}
+      const size_t g0 = (size_t)(cons.item % cons.nchunk) * KC;
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb) {
+        const int r = 8 * jb + r4;
+        if (r >= cons.t.nrows) continue;
+        const int row = xrow(a, cons.t, r);
+        if (active && !active[row % band_mod]) continue;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int g = gw + 8 * gb + 2 * c4 + h;
-          if (g >= a.nbp) continue;
-          const size_t idx = (size_t)row * a.nbp + g;
-          const double2 x = (ca != 0.0) ? Xin[idx] : make_double2(0.0, 0.0);
-          Y[idx] = make_double2(ca * x.x + cb * dr[jb][gb][h], ca * x.y + cb * di[jb][gb][h]);
+          const int gl = 8 * w + 2 * c4 + h;
+          const double2 x = want_x ? xs[r * RSX + gl] : make_double2(0.0, 0.0);
+          Y[(size_t)row * a.nbp + g0 + gl] =
+              make_double2(ca * x.x + cb * dr[jb][h], ca * x.y + cb * di[jb][h]);
         }
+      }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    ++seq;
+    cons.next(a);
   }
 }
+
+// ---------------------------------------------------------------------------
+static int proj_configure() {
+  static bool done = false;
+  if (done) return PWB_OK;
+  PWB_CUDA(cudaFuncSetAttribute(k_proj_coef, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kCoefSmem));
+  PWB_CUDA(cudaFuncSetAttribute(k_proj_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kApplySmem));
+  done = true;
+  return PWB_OK;
+}
+
+static int nsplit_max(int nbp) { return std::max(1, std::min(kSM, nbp / KC)); }
 
 int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int>& nocc,
               int nbp, cudaStream_t st, bool async) {
+  PWB_TRY(proj_configure());
+  if (nbp % KC) return fail(PWB_ERR_UNSUPPORTED, "projector: row stride not a multiple of 64");
   pl.tiles.clear();
   pl.max_tiles = 0;
   const int n = (int)row_k.size();
@@ -301,7 +556,7 @@ int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int
   pl.nrows = n;
   pl.mtiles = std::max(1, (maxocc + CM - 1) / CM);
   const int ntiles = (int)pl.tiles.size();
-  pl.nsplit = std::max(1, std::min(kCoefCtas, nbp / (16 * CW)));   // upper bound
+  pl.nsplit = nsplit_max(nbp);   // upper bound; the live count is chosen on the device
   PWB_TRY(pl.dtiles.ensure(std::max<size_t>(1, pl.tiles.size()) * sizeof(ProjTile)));
   if (!pl.tiles.empty()) {
     if (async) {
@@ -331,11 +586,13 @@ size_t proj_part_elems(const ProjPlan& pl) {
 }
 
 int proj_plan_device(ProjPlan& pl, int max_tiles, int maxocc, int nbp) {
+  PWB_TRY(proj_configure());
+  if (nbp % KC) return fail(PWB_ERR_UNSUPPORTED, "projector: row stride not a multiple of 64");
   pl.tiles.clear();
   pl.max_tiles = max_tiles;
   pl.nrows = max_tiles * TR;
   pl.mtiles = std::max(1, (maxocc + CM - 1) / CM);
-  pl.nsplit = std::max(1, std::min(kCoefCtas, nbp / (16 * CW)));   // upper bound
+  pl.nsplit = nsplit_max(nbp);
   PWB_TRY(pl.dtiles.ensure(std::max<size_t>(1, max_tiles) * sizeof(ProjTile)));
   const size_t ntm = (size_t)std::max(1, max_tiles) * pl.mtiles;
   PWB_TRY(pl.counters.ensure(ntm * sizeof(unsigned)));
@@ -350,9 +607,10 @@ int proj_coeffs(const ProjPlan& pl, ProjArgs a, const double2* X, double2* part,
   a.tiles = reinterpret_cast<const ProjTile*>(pl.dtiles.ptr);
   a.nrows_total = pl.nrows;
   const long items = (long)cap * pl.mtiles * pl.nsplit;
-  const int grid = (int)std::min<long>(items, kCoefCtas);
-  k_proj_coef<<<grid, CW * 32, 0, st>>>(a, X, (int)pl.tiles.size(), cap, pl.mtiles, pl.nsplit,
-                                        part, C, reinterpret_cast<unsigned*>(pl.counters.ptr));
+  const int grid = (int)std::min<long>(items, kSM);
+  k_proj_coef<<<grid, (NW + 1) * 32, kCoefSmem, st>>>(a, X, (int)pl.tiles.size(), cap, pl.mtiles,
+                                                pl.nsplit, part, C,
+                                                reinterpret_cast<unsigned*>(pl.counters.ptr));
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -363,256 +621,12 @@ int proj_apply(const ProjPlan& pl, ProjArgs a, const double2* C, const double2* 
   if (cap == 0) return PWB_OK;
   a.tiles = reinterpret_cast<const ProjTile*>(pl.dtiles.ptr);
   a.nrows_total = pl.nrows;
-  const long items = (long)cap * ((a.nbp + AG - 1) / AG);
-  const int grid = (int)std::min<long>(items, kApplyCtas);
-  k_proj_apply<<<grid, AW * 32, 0, st>>>(a, C, Xin, Y, ca, cb, active,
-                                         band_mod > 0 ? band_mod : 1, (int)pl.tiles.size());
+  const long items = (long)cap * (a.nbp / KC);
+  const int grid = (int)std::min<long>(items, kSM);
+  k_proj_apply<<<grid, (NW + 1) * 32, kApplySmem, st>>>(a, C, Xin, Y, ca, cb, active,
+                                                  band_mod > 0 ? band_mod : 1,
+                                                  (int)pl.tiles.size());
   PWB_LAUNCH_CHECK();
-  return PWB_OK;
-}
-
-// ---------------------------------------------------------------------------
-// Fused Q in ONE launch with a thread-block cluster per row tile:
-//   CTA c of the cluster owns g in [c L, (c+1) L);
-//   phase 1: partial C = Phi^H X over its g range (DMMA), warp-reduced in smem;
-//   cluster barrier; every CTA sums the CS partials through DSMEM in rank
-//   order (deterministic) -> full C in its own smem; cluster barrier;
-//   phase 2: Y = ca X + cb Phi C on its g range with C read from smem.
-// No global partial buffer, no atomics, one launch instead of two.
-}  // namespace pwb
-
-#include <cooperative_groups.h>
-
-namespace pwb {
-
-constexpr int QW = 8;          // warps per CTA
-constexpr int QCS = 8;         // CTAs per cluster (g split)
-
-__global__ void __launch_bounds__(QW * 32) k_proj_q(ProjArgs a, const double2* __restrict__ Xin,
-                                                    double2* __restrict__ Y, double ca, double cb,
-                                                    const int* __restrict__ active, int band_mod,
-                                                    int glen) {
-  namespace cgp = cooperative_groups;
-  cgp::cluster_group cluster = cgp::this_cluster();
-  extern __shared__ double2 qsm[];
-  const int tile = blockIdx.x / QCS;
-  const int crank = (int)cluster.block_rank();
-  if (a.ntiles && tile >= *a.ntiles) return;   // whole cluster exits together
-  const ProjTile t = a.tiles[tile];
-  const int nocc = a.nocc[t.k];
-  const int ldm = ((a.ldc + 31) / 32) * 32;    // m capacity of the smem C blocks
-  double2* red = qsm;                          // [QW/2][CM][TR]
-  double2* cpart = red + (QW / 2) * CM * TR;   // [ldm][TR] this CTA's partial
-  double2* cfull = cpart + ldm * TR;           // [ldm][TR] cluster sum
-  const double2* phi = a.phi + (size_t)a.off[t.k] * a.nbp;
-  const int g0 = crank * glen;
-  const int g1 = min(a.nbp, g0 + glen);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r4 = lane >> 2, c4 = lane & 3;
-
-  const double2* xrw[2];
-  bool xok[2];
-#pragma unroll
-  for (int nb = 0; nb < 2; ++nb) {
-    const int r = 8 * nb + r4;
-    xok[nb] = r < t.nrows;
-    xrw[nb] = Xin + (size_t)(xok[nb] ? (a.rows ? a.rows[t.row0 + r] : t.row0 + r) : 0) * a.nbp;
-  }
-  // ---- phase 1: partial C over this CTA's g range, 32 m at a time
-  for (int m0 = 0; m0 < nocc; m0 += CM) {
-    const double2* prow[4];
-    bool pok[4];
-#pragma unroll
-    for (int ma = 0; ma < 4; ++ma) {
-      const int m = m0 + 8 * ma + r4;
-      pok[ma] = m < nocc;
-      prow[ma] = phi + (size_t)(pok[ma] ? m : 0) * a.nbp;
-    }
-    double cr[4][2][2], ci[4][2][2];
-#pragma unroll
-    for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
-        cr[ma][nb][0] = cr[ma][nb][1] = 0.0;
-        ci[ma][nb][0] = ci[ma][nb][1] = 0.0;
-      }
-    constexpr int NP = 4;
-    for (int gb = g0 + 4 * w; gb < g1; gb += 4 * QW * NP) {
-      double2 av[NP][4], bv[NP][2];
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-        const int gg = gb + 4 * QW * u + c4;
-        const bool gok = gg < g1;
-#pragma unroll
-        for (int ma = 0; ma < 4; ++ma)
-          av[u][ma] = (gok && pok[ma]) ? __ldg(&prow[ma][gg]) : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-          bv[u][nb] = (gok && xok[nb]) ? xrw[nb][gg] : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-#pragma unroll
-        for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-          for (int nb = 0; nb < 2; ++nb) {
-            dmma(cr[ma][nb][0], cr[ma][nb][1], av[u][ma].x, bv[u][nb].x);
-            dmma(ci[ma][nb][0], ci[ma][nb][1], av[u][ma].x, bv[u][nb].y);
-          }
-#pragma unroll
-        for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-          for (int nb = 0; nb < 2; ++nb) {
-            dmma(cr[ma][nb][0], cr[ma][nb][1], av[u][ma].y, bv[u][nb].y);
-            dmma(ci[ma][nb][0], ci[ma][nb][1], -av[u][ma].y, bv[u][nb].x);
-          }
-      }
-    }
-    // fixed-order warp reduction -> cpart[m0 + m][r]
-    if (w >= QW / 2) {
-#pragma unroll
-      for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            red[((w - QW / 2) * CM + 8 * ma + r4) * TR + 8 * nb + 2 * c4 + h] =
-                make_double2(cr[ma][nb][h], ci[ma][nb][h]);
-    }
-    __syncthreads();
-    if (w < QW / 2) {
-#pragma unroll
-      for (int ma = 0; ma < 4; ++ma)
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            double2& slot = red[(w * CM + 8 * ma + r4) * TR + 8 * nb + 2 * c4 + h];
-            slot = make_double2(cr[ma][nb][h] + slot.x, ci[ma][nb][h] + slot.y);
-          }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < CM * TR; i += QW * 32) {
-      double2 s = red[i];
-#pragma unroll
-      for (int q = 1; q < QW / 2; ++q) s = cadd(s, red[q * CM * TR + i]);
-      cpart[m0 * TR + i] = s;
-    }
-    __syncthreads();
-  }
-  // ---- cluster reduction through DSMEM, rank order
-  cluster.sync();
-  for (int i = threadIdx.x; i < nocc * TR; i += QW * 32) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int c = 0; c < QCS; ++c) {
-      const double2* rp = cluster.map_shared_rank(cpart, c);
-      s = cadd(s, rp[i]);
-    }
-    cfull[i] = s;
-  }
-  cluster.sync();   // no CTA may leave while its cpart is still being read
-  // ---- phase 2: Y = ca X + cb Phi C on this CTA's g range
-  for (int gw = g0 + 32 * w; gw < g1; gw += 32 * QW) {
-    double dr[2][4][2], di[2][4][2];
-#pragma unroll
-    for (int jb = 0; jb < 2; ++jb)
-#pragma unroll
-      for (int gb = 0; gb < 4; ++gb) {
-        dr[jb][gb][0] = dr[jb][gb][1] = 0.0;
-        di[jb][gb][0] = di[jb][gb][1] = 0.0;
-      }
-    constexpr int NP = 8;
-    for (int mb = 0; mb < nocc; mb += 4 * NP) {
-      double2 av[NP][2], bv[NP][4];
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-        const int mm = mb + 4 * u + c4;
-        const bool mok = mm < nocc;
-#pragma unroll
-        for (int jb = 0; jb < 2; ++jb)   // A[j = r4][k = c4] = C[row j][m]
-          av[u][jb] = mok ? cfull[mm * TR + 8 * jb + r4] : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int gb = 0; gb < 4; ++gb) {
-          const int g = gw + 8 * gb + r4;   // B[k = c4][n = r4] = Phi[m][g]
-          bv[u][gb] = (mok && g < g1) ? __ldg(&phi[(size_t)mm * a.nbp + g])
-                                      : make_double2(0.0, 0.0);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-#pragma unroll
-        for (int jb = 0; jb < 2; ++jb)
-#pragma unroll
-          for (int gb = 0; gb < 4; ++gb) {
-            dmma(dr[jb][gb][0], dr[jb][gb][1], av[u][jb].x, bv[u][gb].x);
-            dmma(di[jb][gb][0], di[jb][gb][1], av[u][jb].x, bv[u][gb].y);
-          }
-#pragma unroll
-        for (int jb = 0; jb < 2; ++jb)
-#pragma unroll
-          for (int gb = 0; gb < 4; ++gb) {
-            dmma(dr[jb][gb][0], dr[jb][gb][1], -av[u][jb].y, bv[u][gb].y);
-            dmma(di[jb][gb][0], di[jb][gb][1], av[u][jb].y, bv[u][gb].x);
-          }
-      }
-    }
-#pragma unroll
-    for (int jb = 0; jb < 2; ++jb) {
-      const int r = 8 * jb + r4;
-      if (r >= t.nrows) continue;
-      const int row = a.rows ? a.rows[t.row0 + r] : t.row0 + r;
-      if (active && !active[row % band_mod]) continue;
-#pragma unroll
-      for (int gb = 0; gb < 4; ++gb)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int g = gw + 8 * gb + 2 * c4 + h;
-          if (g >= g1) continue;
-          const size_t idx = (size_t)row * a.nbp + g;
-          const double2 x = (ca != 0.0) ? Xin[idx] : make_double2(0.0, 0.0);
-          Y[idx] = make_double2(ca * x.x + cb * dr[jb][gb][h], ca * x.y + cb * di[jb][gb][h]);
-        }
-    }
-  }
-}
-
-size_t proj_q_smem(int ldc) {
-  const int ldm = ((ldc + 31) / 32) * 32;
-  return ((size_t)(QW / 2) * CM * TR + 2 * (size_t)ldm * TR) * sizeof(double2);
-}
-
-int proj_q(const ProjPlan& pl, ProjArgs a, const double2* Xin, double2* Y, double ca, double cb,
-           const int* active, int band_mod, cudaStream_t st) {
-  const int nt = plan_tiles(pl);
-  if (nt == 0) return PWB_OK;
-  a.tiles = reinterpret_cast<const ProjTile*>(pl.dtiles.ptr);
-  a.nrows_total = pl.nrows;
-  int glen = (a.nbp + QCS - 1) / QCS;
-  glen = ((glen + 31) / 32) * 32;
-  const size_t smem = proj_q_smem(a.ldc);
-  static bool configured = false;
-  static size_t configured_smem = 0;
-  if (!configured || smem > configured_smem) {
-    PWB_CUDA(cudaFuncSetAttribute(k_proj_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)std::max<size_t>(smem, 48 * 1024)));
-    configured = true;
-    configured_smem = std::max<size_t>(smem, 48 * 1024);
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(nt * QCS), 1, 1);
-  cfg.blockDim = dim3(QW * 32, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = QCS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  PWB_CUDA(cudaLaunchKernelEx(&cfg, k_proj_q, a, Xin, Y, ca, cb, active,
-                              band_mod > 0 ? band_mod : 1, glen));
-  count_launch();
   return PWB_OK;
 }
 

@@ -8,11 +8,11 @@
 
 namespace pwb {
 
-constexpr int kProjTileRows = 16;   // rows per projector tile (2 DMMA n-fragments)
+constexpr int kProjTileRows = 16;   // rows per projector tile (<= 2 DMMA n-fragments)
 
 struct ProjTile {
   int row0;   // first row of X in this tile
-  int nrows;  // <= 32, all in k block `k`
+  int nrows;  // <= kProjTileRows, all in k block `k`
   int k;
 };
 
@@ -45,11 +45,6 @@ inline int plan_tiles(const ProjPlan& pl) {
   return pl.max_tiles > 0 ? pl.max_tiles : (int)pl.tiles.size();
 }
 
-// fused one-launch Q (cluster of 8 CTAs per row tile, DSMEM reduction of C):
-// Y = ca X + cb Phi (Phi^H X), rows with active[row % band_mod] == 0 untouched
-int proj_q(const ProjPlan& pl, ProjArgs a, const double2* Xin, double2* Y, double ca, double cb,
-           const int* active, int band_mod, cudaStream_t st);
-
 // capacity plan whose tile list (<= max_tiles entries) is written on the device;
 // launches cover max_tiles and CTAs beyond the device count ProjArgs::ntiles exit
 int proj_plan_device(ProjPlan& pl, int max_tiles, int maxocc, int nbp);
@@ -61,10 +56,6 @@ int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int
               cudaStream_t st = nullptr, bool async = false);
 // scratch (complex elements) needed by proj_coeffs for this plan / any plan of <= nrows rows
 size_t proj_part_elems(const ProjPlan& pl);
-inline size_t proj_part_bound(int nrows, int ldc) {
-  const size_t mt = (size_t)(ldc + 31) / 32;
-  return (2 * (size_t)kSM + (size_t)nrows * mt + 64) * mt * 32 * 16 + 32 * 16;
-}
 // C = Phi^H X   (part: nsplit * nrows * ldc scratch)
 int proj_coeffs(const ProjPlan& pl, ProjArgs a, const double2* X, double2* part, double2* C,
                 cudaStream_t st);

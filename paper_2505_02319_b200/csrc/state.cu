@@ -387,38 +387,51 @@ int pwb_project_generic(int nb, int nocc, const double* phi, int ncol, double* x
   if (nb < 1 || nocc < 1 || ncol < 0) return fail(PWB_ERR_VALUE, "bad projector sizes");
   if (ncol == 0) return PWB_OK;
   static thread_local ProjPlan plan;
-  static thread_local DevBuf part, cmat, meta;
+  static thread_local DevBuf part, cmat, meta, pphi, px;
   static thread_local std::vector<int> key;
+  const int nbp = (nb + 63) / 64 * 64;   // the projector streams rows in 64-coefficient chunks
   std::vector<int> rk(ncol, 0), nocc_v(1, nocc);
   std::vector<int> k2 = {nb, nocc, ncol};
   if (key != k2) {
-    PWB_TRY(proj_plan(plan, rk, nocc_v, nb));
+    PWB_TRY(proj_plan(plan, rk, nocc_v, nbp));
+    PWB_TRY(meta.ensure(2 * sizeof(int)));
+    int hm[2] = {0, nocc};
+    PWB_CUDA(cudaMemcpy(meta.ptr, hm, 2 * sizeof(int), cudaMemcpyHostToDevice));
     key = k2;
   }
-  PWB_TRY(meta.ensure(2 * sizeof(int)));
-  int hm[2] = {0, nocc};
-  PWB_CUDA(cudaMemcpy(meta.ptr, hm, 2 * sizeof(int), cudaMemcpyHostToDevice));
   PWB_TRY(part.ensure(proj_part_elems(plan) * sizeof(double2)));
   PWB_TRY(cmat.ensure((size_t)ncol * nocc * sizeof(double2)));
+  const double2* P = reinterpret_cast<const double2*>(phi);
+  double2* X = reinterpret_cast<double2*>(x);
+  double2* XP = X;
+  const size_t row = (size_t)nb * sizeof(double2), rowp = (size_t)nbp * sizeof(double2);
+  if (nbp != nb) {   // zero-padded copies (pads must be exactly zero)
+    PWB_TRY(pphi.ensure((size_t)nocc * rowp));
+    PWB_TRY(px.ensure((size_t)ncol * rowp));
+    PWB_CUDA(cudaMemsetAsync(pphi.ptr, 0, (size_t)nocc * rowp, nullptr));
+    PWB_CUDA(cudaMemsetAsync(px.ptr, 0, (size_t)ncol * rowp, nullptr));
+    PWB_CUDA(cudaMemcpy2DAsync(pphi.ptr, rowp, phi, row, row, nocc, cudaMemcpyDeviceToDevice,
+                               nullptr));
+    PWB_CUDA(cudaMemcpy2DAsync(px.ptr, rowp, x, row, row, ncol, cudaMemcpyDeviceToDevice,
+                               nullptr));
+    P = as<double2>(pphi);
+    XP = as<double2>(px);
+  }
   ProjArgs a;
-  a.phi = reinterpret_cast<const double2*>(phi);
+  a.phi = P;
   a.off = as<int>(meta);
   a.nocc = as<int>(meta) + 1;
   a.tiles = nullptr;
-  a.nbp = nb;
+  a.nbp = nbp;
   a.ldc = nocc;
   a.nrows_total = ncol;
   a.rows = nullptr;
   a.ntiles = nullptr;
-  double2* X = reinterpret_cast<double2*>(x);
-  if (getenv("PWB_PROJ_FUSED")) {   // cluster/DSMEM one-launch variant (comparison)
-    PWB_TRY(proj_q(plan, a, X, X, 1.0, -1.0, nullptr, ncol, nullptr));
-  } else {
-    PWB_TRY(proj_coeffs(plan, a, X, as<double2>(part), as<double2>(cmat), nullptr));
-    PWB_TRY(proj_apply(plan, a, as<double2>(cmat), X, X, 1.0, -1.0, nullptr, ncol, nullptr));
-  }
-  PWB_CUDA(cudaStreamSynchronize(nullptr));
-  return PWB_OK;
+  PWB_TRY(proj_coeffs(plan, a, XP, as<double2>(part), as<double2>(cmat), nullptr));
+  PWB_TRY(proj_apply(plan, a, as<double2>(cmat), XP, XP, 1.0, -1.0, nullptr, ncol, nullptr));
+  if (XP != X)
+    PWB_CUDA(cudaMemcpy2DAsync(x, row, XP, rowp, row, ncol, cudaMemcpyDeviceToDevice, nullptr));
+  return PWB_OK;   // asynchronous on the legacy default stream
 }
 
 int pwb_project_host(int nb, int nocc, const double* phi_host, int ncol, double* x_host) {
