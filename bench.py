@@ -359,7 +359,7 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = _lib.launch_count()
-    total_ms, n_ham, iters = 0.0, 0, []
+    total_ms, n_ham, iters, step_ms = 0.0, 0, [], []
     barrier()
     for _ in range(args.steps):
         flush.zero_()
@@ -369,7 +369,8 @@ def main():
         res = solve_dyson(gs, dv0_t, sync_timing=False, **kw)
         e1.record()
         torch.cuda.synchronize()
-        total_ms += e0.elapsed_time(e1)
+        step_ms.append(e0.elapsed_time(e1))
+        total_ms += step_ms[-1]
         n_ham += res.n_ham
         iters.append(res.iterations)
     barrier()
@@ -382,6 +383,7 @@ def main():
     torch.cuda.synchronize()
     solve_dyson(gs, dv0_t, sync_timing=False, **kw)
     prof = _lib.profile_read()
+    hist = _lib.profile_hist()
     _lib.profile(False)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -425,8 +427,12 @@ def main():
             "dtype": "f64/c128", "data": "synthetic",
             "config": dict(workload_desc(args.config, gs, params), parallelism=f"kn-shard{world}"),
             "n_ham_per_solve": n_ham / args.steps, "gmres_iterations": iters,
+            "step_ms": [round(t, 3) for t in step_ms],
             "gpu_launches": int(launches), "clocks": clk, "e2e": e2e,
-            "roofline": roofline_from_profile(prof, gs)}
+            "roofline": roofline_from_profile(prof, gs),
+            "kernel_ms_by_live_rows": {
+                cat: {f">={1 << b}": [round(ms, 2), n] for b, ms, n in rows}
+                for cat, rows in hist.items() if cat in ("ham_apply", "projector", "cg_vector")}}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(gs, dv0, params, args.cpu_budget)
     print(json.dumps(line))

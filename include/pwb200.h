@@ -61,6 +61,8 @@ int pwb_grid_set_stream(pwb_grid* grid, void* stream);
 int pwb_profile_enable(int on);
 int pwb_profile_reset(void);
 int pwb_profile_read(double* ms, long long* count, long long* units);
+/* the same split as a histogram over floor(log2(live rows)): ms[cat * 16 + bucket] */
+int pwb_profile_hist(double* ms, long long* count);
 
 /* ---- grid / FFT plan:  FourierGrids (pwbasis.py:95-224) --------------------
  * nk k-point spheres sharing one (nx,ny,nz) cube.  g_int: concatenation over

@@ -13,7 +13,9 @@ import threading
 from .errors import ConfigurationError, DeviceError, NonConvergenceError, PwdysonError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpwb200.so")
+# PWB200_VARIANT selects a performance-experiment build (build.py --variant); default = product
+LIB_PATH = os.path.join(HERE, f"libpwb200_{os.environ['PWB200_VARIANT']}.so"
+                        if os.environ.get("PWB200_VARIANT") else "libpwb200.so")
 
 PWB_OK, PWB_ERR_VALUE, PWB_ERR_CONFIG, PWB_ERR_NONCONV = 0, 1, 2, 3
 PWB_ERR_CUDA, PWB_ERR_UNSUPPORTED, PWB_ERR_NOMEM = 4, 5, 6
@@ -60,6 +62,7 @@ SIGNATURES = {
     "pwb_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "pwb_profile_reset": (ctypes.c_int, []),
     "pwb_profile_read": (ctypes.c_int, [_vp, _vp, _vp]),
+    "pwb_profile_hist": (ctypes.c_int, [_vp, _vp]),
     "pwb_vec_dot": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
     "pwb_vec_axpy": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_double, _vp, _vp]),
     "pwb_arnoldi_mgs": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
@@ -138,6 +141,17 @@ def profile_read():
     load().pwb_profile_read(ctypes.c_void_p(ms.ctypes.data), ctypes.c_void_p(cnt.ctypes.data),
                             ctypes.c_void_p(units.ctypes.data))
     return {name: (float(ms[i]), int(cnt[i]), int(units[i]))
+            for i, name in enumerate(PROFILE_CATEGORIES)}
+
+
+def profile_hist():
+    """{category: [(bucket, ms, launch groups)]}: time split by log2(live rows)."""
+    import numpy as np
+    ms = np.zeros(8 * 16)
+    cnt = np.zeros(8 * 16, dtype=np.int64)
+    load().pwb_profile_hist(ctypes.c_void_p(ms.ctypes.data), ctypes.c_void_p(cnt.ctypes.data))
+    return {name: [(b, float(ms[i * 16 + b]), int(cnt[i * 16 + b])) for b in range(16)
+                   if cnt[i * 16 + b]]
             for i, name in enumerate(PROFILE_CATEGORIES)}
 
 

@@ -1,6 +1,10 @@
 """Build libpwb200.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
-Usage:  python -m paper_2505_02319_b200.build [--force]
+Usage:  python -m paper_2505_02319_b200.build [--force] [--variant NAME -DMACRO=VALUE ...]
+
+A variant (performance experiments only) is built into libpwb200_<NAME>.so and
+selected at load time with PWB200_VARIANT=<NAME>; the default library is the
+product.
 """
 
 import os
@@ -23,27 +27,32 @@ def _nvcc():
     return "nvcc"
 
 
-def _stale():
-    if not os.path.exists(LIB):
+def lib_path(variant=""):
+    return os.path.join(HERE, f"libpwb200_{variant}.so" if variant else "libpwb200.so")
+
+
+def _stale(lib):
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(HERE, "..", "include", "pwb200.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, variant="", defines=()):
     """Compile every CUDA source for sm_100a and link libpwb200.so next to this file."""
-    if not force and not _stale():
-        return LIB
+    lib = lib_path(variant)
+    if not force and not _stale(lib):
+        return lib
     nvcc = _nvcc()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" + (f"_{variant}" if variant else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, *defines, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     for src, p in procs:
@@ -52,15 +61,19 @@ def build(force=False, verbose=False):
             raise RuntimeError(f"nvcc failed on {src}:\n{out.decode()}")
         if verbose and out:
             print(out.decode())
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
            "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    argv = sys.argv[1:]
+    var = argv[argv.index("--variant") + 1] if "--variant" in argv else ""
+    defs = tuple(a for a in argv if a.startswith("-D"))
+    print(build(force="--force" in argv or bool(var), verbose="-v" in argv, variant=var,
+                defines=defs))

@@ -50,6 +50,7 @@ __device__ __forceinline__ double minv(const GridDev& g, int k, int s, double ps
 __global__ void __launch_bounds__(NTC) k_cg_init(GridDev g, CgScalars sc, int n,
                                                  const double2* __restrict__ rhs,
                                                  double2* __restrict__ xr, double2* __restrict__ z) {
+  pdl_wait();
   const int row = blockIdx.x;
   const int k = sc.row_k[row];
   const double ps = sc.pshift[row];
@@ -76,6 +77,7 @@ __global__ void __launch_bounds__(NTC) k_cg_init2(GridDev g, CgScalars sc, int n
                                                   const double2* __restrict__ xr,
                                                   const double2* __restrict__ z,
                                                   double2* __restrict__ p) {
+  pdl_wait();
   __shared__ double red[NTC / 32 + 1];
   const int row = blockIdx.x;
   const double2* r = xr + (size_t)(n + row) * g.nbp;
@@ -99,6 +101,7 @@ __global__ void __launch_bounds__(NTC) k_cg_alpha(GridDev g, CgScalars sc, int n
                                                   double2* __restrict__ xr,
                                                   const int* __restrict__ rows,
                                                   const int* __restrict__ nact) {
+  pdl_wait();
   __shared__ double red[NTC / 32 + 1];
   if (nact && (int)blockIdx.x >= *nact) return;
   const int row = rows ? rows[blockIdx.x] : blockIdx.x;
@@ -135,6 +138,7 @@ __global__ void __launch_bounds__(NTC) k_cg_resid(GridDev g, CgScalars sc, int n
                                                   const int* __restrict__ rows,
                                                   const int* __restrict__ nact,
                                                   int* __restrict__ counters) {
+  pdl_wait();
   __shared__ double red[NTC / 32 + 1];
   if (nact && (int)blockIdx.x >= *nact) return;
   const int row = rows ? rows[blockIdx.x] : blockIdx.x;
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(NTC) k_cg_beta(GridDev g, CgScalars sc, int n,
                                                  double2* __restrict__ p,
                                                  const int* __restrict__ rows,
                                                  const int* __restrict__ nact) {
+  pdl_wait();
   __shared__ double red[NTC / 32 + 1];
   if (nact && (int)blockIdx.x >= *nact) return;
   const int row = rows ? rows[blockIdx.x] : blockIdx.x;
@@ -197,6 +202,7 @@ __global__ void __launch_bounds__(NTC) k_cg_beta(GridDev g, CgScalars sc, int n,
 }
 
 __global__ void k_zero2(int* c) {
+  pdl_wait();
   c[0] = 0;
   c[1] = 0;
 }
@@ -206,6 +212,7 @@ __global__ void k_zero2(int* c) {
 // Rows are in k-block order, so each k's active rows are contiguous.
 __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __restrict__ active,
                                                   const int* __restrict__ row_k, IterCtl ctl) {
+  pdl_wait();
   __shared__ int scan[1024];
   __shared__ int kcnt[kMaxK], kstart[kMaxK], ktile[kMaxK];
   __shared__ int carry;
@@ -284,6 +291,8 @@ ProjArgs proj_args(pwb_state* st) {
   a.nrows_total = 0;
   a.rows = nullptr;
   a.ntiles = nullptr;
+  a.phic = as<double2>(st->phic);
+  a.phic_off = as<int>(st->phic_meta) + 2 * st->nk;
   return a;
 }
 
@@ -297,7 +306,7 @@ int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* activ
   cudaEvent_t e = prof().begin(s);
   PWB_TRY(proj_coeffs(pl, a, X, part, cmat, s));
   PWB_TRY(proj_apply(pl, a, cmat, X, X, 1.0, -1.0, active, band_mod, s));
-  prof().end(PROF_Q, e, s, pl.nrows);
+  prof().end(PROF_Q, e, s, prof().rows_hint > 0 ? prof().rows_hint : pl.nrows);
   return PWB_OK;
 }
 
@@ -399,7 +408,7 @@ static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s) {
   g->stream = s;
   int status = PWB_OK;
   do {
-    k_compact<<<1, 1024, 0, s>>>(n, st->nk, cg.s.active, cg.s.row_k, cg.ctl);
+    (void)launch_k(k_compact, 1, 1024, 0, s, n, st->nk, cg.s.active, cg.s.row_k, cg.ctl);
     count_launch();
     if ((status = project_rows(st, cg.pa, p, cg.s.active, n, rows, part, cmat, s, cg.ctl.hdr + 1)))
       break;
@@ -412,22 +421,22 @@ static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s) {
                                cg.ctl.hdr + 1)))
       break;
     cudaEvent_t ec = prof().begin(s);
-    k_cg_alpha<<<n, NTC, 0, s>>>(g->dev, cg.s, n, p, ap, xr, rows, nact);
+    (void)launch_k(k_cg_alpha, n, NTC, 0, s, g->dev, cg.s, n, p, ap, xr, rows, nact);
     count_launch();
     prof().end(PROF_CG, ec, s, cg.prof_rows);
     if ((status = project_rows(st, cg.pb, xr, cg.s.active, n, cg.ctl.rows2, part, cmat, s,
                                cg.ctl.hdr + 2)))
       break;
     ec = prof().begin(s);
-    k_zero2<<<1, 1, 0, s>>>(cg.ctl.hdr + 3);
-    k_cg_resid<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, rows, nact, cg.ctl.hdr + 3);
+    (void)launch_k(k_zero2, 1, 1, 0, s, cg.ctl.hdr + 3);
+    (void)launch_k(k_cg_resid, n, NTC, 0, s, g->dev, cg.s, n, xr, z, rows, nact, cg.ctl.hdr + 3);
     count_launch(2);
     prof().end(PROF_CG, ec, s, cg.prof_rows);
     cudaMemcpyAsync(cg.h_hdr, cg.ctl.hdr, 8 * sizeof(int), cudaMemcpyDeviceToHost, s);
     if ((status = project_rows(st, cg.pa, z, cg.s.active, n, rows, part, cmat, s, cg.ctl.hdr + 1)))
       break;
     ec = prof().begin(s);
-    k_cg_beta<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, p, rows, nact);
+    (void)launch_k(k_cg_beta, n, NTC, 0, s, g->dev, cg.s, n, xr, z, p, rows, nact);
     count_launch();
     prof().end(PROF_CG, ec, s, cg.prof_rows);
     cudaError_t e = cudaGetLastError();
@@ -476,11 +485,11 @@ int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max
   double2* xr = as<double2>(cg.xr);
   double2* z = as<double2>(cg.z);
   double2* p = as<double2>(cg.p);
-  k_cg_init<<<n, NTC, 0, s>>>(g->dev, cg.s, n, as<double2>(cg.rhs), xr, z);
+  (void)launch_k(k_cg_init, n, NTC, 0, s, g->dev, cg.s, n, as<double2>(cg.rhs), xr, z);
   PWB_LAUNCH_CHECK();
   PWB_TRY(project_rows(st, cg.plan1, z, nullptr, n, nullptr, as<double2>(cg.part),
                        as<double2>(cg.cmat), s, nullptr));
-  k_cg_init2<<<n, NTC, 0, s>>>(g->dev, cg.s, n, xr, z, p);
+  (void)launch_k(k_cg_init2, n, NTC, 0, s, g->dev, cg.s, n, xr, z, p);
   PWB_LAUNCH_CHECK();
   const size_t wbytes = (size_t)n * g->nxa * g->nyz * sizeof(double2);
   if (g->wbuf.bytes < wbytes || !g->wbuf.ptr) {
@@ -503,6 +512,7 @@ int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max
       PWB_CUDA(cudaGraphLaunch(cg.exec, s));
       count_launch((int)g_iter_launches);
     } else {
+      prof().rows_hint = cg.prof_rows;
       PWB_TRY(enqueue_iteration(st, cg, s));
     }
     PWB_CUDA(cudaStreamSynchronize(s));
@@ -510,6 +520,7 @@ int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max
     cg.prof_rows = cg.h_hdr[3];
     if (cg.h_hdr[3] == 0) break;   // no row still iterating
   }
+  prof().rows_hint = 0;
   const bool failed = cg.h_hdr[4] != 0;
   std::vector<int> its(n);
   std::vector<double> res(n);

@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(NTA) k_drho_partial(GridDev g, int nband, int 
                                                       const double* __restrict__ c2,
                                                       const double* __restrict__ c1,
                                                       double* __restrict__ partial) {
+  pdl_wait();
   extern __shared__ double2 sm[];
   const int T = g.tile, Tp = g.tilep, nx = g.nx, nyz = g.nyz;
   const int t0 = blockIdx.x * T;
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(NTA) k_drho_partial(GridDev g, int nband, int 
 
 __global__ void k_drho_reduce(int n, int nchunk, const double* __restrict__ partial,
                               double* __restrict__ drho) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = partial[i];
@@ -75,6 +77,7 @@ __global__ void k_drho_reduce(int n, int nchunk, const double* __restrict__ part
 // out[i] = sum_b |psi_b(i)|^2  (or (Re psi_b)^2); max taken by k_max_reduce
 __global__ void k_row_sq(int n, int nband, const double2* __restrict__ psir, int real_part,
                          double* __restrict__ out) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
@@ -86,6 +89,7 @@ __global__ void k_row_sq(int n, int nband, const double2* __restrict__ psir, int
 }
 
 __global__ void k_max_reduce(int n, const double* __restrict__ in, double* __restrict__ out) {
+  pdl_wait();
   __shared__ double red[256];
   double m = 0.0;
   for (int i = threadIdx.x; i < n; i += 256) m = fmax(m, in[i]);
@@ -106,7 +110,7 @@ int launch_drho_partial(pwb_grid* g, int nband, const double2* W, const double2*
   const int per = (nband + nchunk - 1) / nchunk;
   dim3 grid(ntile, nchunk);
   pencil_variant(g, [&](auto fx) {
-    k_drho_partial<decltype(fx)><<<grid, NTA, pencil_smem(g), g->stream>>>(
+    (void)launch_k(k_drho_partial<decltype(fx)>, grid, NTA, pencil_smem(g), g->stream, 
         g->dev, nband, per, W, psir, c2, c1, partial);
   });
   PWB_LAUNCH_CHECK();
@@ -114,7 +118,7 @@ int launch_drho_partial(pwb_grid* g, int nband, const double2* W, const double2*
 }
 
 int launch_drho_reduce(pwb_grid* g, int nchunk, const double* partial, double* drho) {
-  k_drho_reduce<<<(g->ng + 255) / 256, 256, 0, g->stream>>>(g->ng, nchunk, partial, drho);
+  (void)launch_k(k_drho_reduce, (g->ng + 255) / 256, 256, 0, g->stream, g->ng, nchunk, partial, drho);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -122,9 +126,9 @@ int launch_drho_reduce(pwb_grid* g, int nchunk, const double* partial, double* d
 int launch_row_norm(pwb_grid* g, int nband, const double2* psir, int real_part, double* out) {
   PWB_TRY(g->tmp_real.ensure((size_t)(g->ng + 1) * sizeof(double)));
   double* sq = as<double>(g->tmp_real);
-  k_row_sq<<<(g->ng + 255) / 256, 256, 0, g->stream>>>(g->ng, nband, psir, real_part, sq);
+  (void)launch_k(k_row_sq, (g->ng + 255) / 256, 256, 0, g->stream, g->ng, nband, psir, real_part, sq);
   PWB_LAUNCH_CHECK();
-  k_max_reduce<<<1, 256, 0, g->stream>>>(g->ng, sq, out);
+  (void)launch_k(k_max_reduce, 1, 256, 0, g->stream, g->ng, sq, out);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }

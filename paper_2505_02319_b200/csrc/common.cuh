@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../../include/pwb200.h"
 
@@ -70,5 +72,32 @@ __host__ __device__ __forceinline__ double2 cmul_isgn(double2 a, double sgn) {
 __host__ __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 
 constexpr int kSM = 148;   // B200 SM count (grid sizing)
+
+// --- programmatic dependent launch (PDL) ---------------------------------------
+// Kernels of the CG iteration are launched with programmatic stream
+// serialisation: the next kernel's launch and prologue overlap the tail of the
+// previous one.  Every kernel launched this way calls pdl_wait() before it
+// touches global memory written or read by its predecessor (so before any
+// global access at all), which also keeps the completion chain transitive.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+extern bool g_pdl;   // false when PWB_NO_PDL is set (A/B measurement)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace pwb

@@ -16,16 +16,20 @@
 namespace pwb {
 
 constexpr int NT = 256;
+#ifndef PWB_FFT_MINB
+#define PWB_FFT_MINB 3   // min resident CTAs per SM for the H-apply kernels (80-register cap; measured best)
+#endif
 
 // ----------------------------------------------------------------------------
 // plane pass, inverse: sphere rows -> W[b][p]
 template <class FY, class FZ>
-__global__ void __launch_bounds__(NT) k_plane_inv(GridDev g, const double2* __restrict__ psi,
+__global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_inv(GridDev g, const double2* __restrict__ psi,
                                                   const double2* __restrict__ psi2,
                                                   const int* __restrict__ band_k, double scale,
                                                   double2* __restrict__ W,
                                                   const int* __restrict__ rows,
                                                   const int* __restrict__ nact) {
+  pdl_wait();
   extern __shared__ double2 sm[];
   if (nact && (int)blockIdx.y >= *nact) return;   // device-side row count (graph replay)
   const int p = blockIdx.x;
@@ -60,13 +64,14 @@ __global__ void __launch_bounds__(NT) k_plane_inv(GridDev g, const double2* __re
 // plane pass, forward: W[b][p] -> sphere rows with epilogue
 //   out[s] = a * F(W)[pp[s]] + (kin[s] - shift[b]) * psi_in[s]
 template <class FY, class FZ>
-__global__ void __launch_bounds__(NT) k_plane_fwd(GridDev g, const double2* __restrict__ W,
+__global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_fwd(GridDev g, const double2* __restrict__ W,
                                                   const int* __restrict__ band_k, double a,
                                                   const double2* __restrict__ psi_in,
                                                   const double* __restrict__ shift,
                                                   double2* __restrict__ out,
                                                   const int* __restrict__ rows,
                                                   const int* __restrict__ nact) {
+  pdl_wait();
   extern __shared__ double2 sm[];
   if (nact && (int)blockIdx.y >= *nact) return;
   const int p = blockIdx.x;
@@ -132,7 +137,8 @@ struct PencilArgs {
 };
 
 template <int IN, int OUT, class FX>
-__global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
+__global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_pencil(GridDev g, PencilArgs a) {
+  pdl_wait();
   extern __shared__ double2 sm[];
   const int T = g.tile, Tp = g.tilep, nyz = g.nyz;
   const int nx = FX::N ? FX::N : g.nx;   // compile-time for the codelet sizes
@@ -206,6 +212,7 @@ __global__ void __launch_bounds__(NT) k_pencil(GridDev g, PencilArgs a) {
 template <class FY, class FZ>
 __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restrict__ Wf, int mode,
                                                    double param, int inverse) {
+  pdl_wait();
   extern __shared__ double2 sm[];
   const int x = blockIdx.x;
   const int v = blockIdx.y;
@@ -255,7 +262,7 @@ int launch_plane_inv(pwb_grid* g, int nband, const int* band_k, const double2* p
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
-    k_plane_inv<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
+    (void)launch_k(k_plane_inv<decltype(fy), decltype(fz)>, grid, NT, plane_smem(g), g->stream, 
         g->dev, psi, nullptr, band_k, scale, W, rows, nact);
   });
   PWB_LAUNCH_CHECK();
@@ -268,7 +275,7 @@ int launch_plane_inv2(pwb_grid* g, int nband, const int* band_k, const double2* 
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
-    k_plane_inv<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
+    (void)launch_k(k_plane_inv<decltype(fy), decltype(fz)>, grid, NT, plane_smem(g), g->stream, 
         g->dev, a, b, band_k, 1.0, W, nullptr, nullptr);
   });
   PWB_LAUNCH_CHECK();
@@ -282,7 +289,7 @@ int launch_plane_fwd(pwb_grid* g, int nband, const int* band_k, const double2* W
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
-    k_plane_fwd<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
+    (void)launch_k(k_plane_fwd<decltype(fy), decltype(fz)>, grid, NT, plane_smem(g), g->stream, 
         g->dev, W, band_k, a, psi_in, shift, out, rows, nact);
   });
   PWB_LAUNCH_CHECK();
@@ -301,6 +308,7 @@ static PencilArgs empty_args() {
 // by the fused V(r) multiply of the pencil pass (coalesced loads)
 __global__ void k_transpose_v(int nx, int nyz, const double* __restrict__ v,
                               double* __restrict__ vt) {
+  pdl_wait();
   __shared__ double tile[32][33];
   const int t0 = blockIdx.x * 32, x0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
@@ -316,7 +324,7 @@ __global__ void k_transpose_v(int nx, int nyz, const double* __restrict__ v,
 
 int launch_transpose_v(pwb_grid* g, const double* v, double* vt) {
   dim3 grid((g->nyz + 31) / 32, (g->nx + 31) / 32);
-  k_transpose_v<<<grid, dim3(32, 8), 0, g->stream>>>(g->nx, g->nyz, v, vt);
+  (void)launch_k(k_transpose_v, grid, dim3(32, 8), 0, g->stream, g->nx, g->nyz, v, vt);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -341,7 +349,7 @@ int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, doub
   a.out_stride = a.in_stride;
   dim3 grid(tiles(g), nband);
   pencil_variant(g, [&](auto fx) {
-    k_pencil<0, 0, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    (void)launch_k(k_pencil<0, 0, decltype(fx)>, grid, NT, pencil_smem(g), g->stream, g->dev, a);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -361,7 +369,7 @@ int launch_pencil_to_cube(pwb_grid* g, int nband, const double2* W, double scale
   a.oscale = scale;
   dim3 grid(tiles(g), nband);
   pencil_variant(g, [&](auto fx) {
-    k_pencil<0, 1, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    (void)launch_k(k_pencil<0, 1, decltype(fx)>, grid, NT, pencil_smem(g), g->stream, g->dev, a);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -380,7 +388,7 @@ int launch_pencil_from_cube(pwb_grid* g, int nband, const double2* in, double2* 
   a.out_stride = (size_t)g->nxa * g->nyz;
   dim3 grid(tiles(g), nband);
   pencil_variant(g, [&](auto fx) {
-    k_pencil<1, 0, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    (void)launch_k(k_pencil<1, 0, decltype(fx)>, grid, NT, pencil_smem(g), g->stream, g->dev, a);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -402,11 +410,11 @@ int launch_full_from_natural(pwb_grid* g, int nvec, const double2* in_c, const d
   dim3 grid(tiles(g), nvec);
   if (in_c)
     pencil_variant(g, [&](auto fx) {
-    k_pencil<1, 0, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    (void)launch_k(k_pencil<1, 0, decltype(fx)>, grid, NT, pencil_smem(g), g->stream, g->dev, a);
   });
   else
     pencil_variant(g, [&](auto fx) {
-    k_pencil<2, 0, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    (void)launch_k(k_pencil<2, 0, decltype(fx)>, grid, NT, pencil_smem(g), g->stream, g->dev, a);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -417,7 +425,7 @@ int launch_full_plane(pwb_grid* g, int nvec, double2* Wf, int mode, double param
   if (nvec == 0) return PWB_OK;
   dim3 grid(g->nx, nvec);
   plane_variant(g, [&](auto fy, auto fz) {
-    k_plane_full<decltype(fy), decltype(fz)><<<grid, NT, plane_smem(g), g->stream>>>(
+    (void)launch_k(k_plane_full<decltype(fy), decltype(fz)>, grid, NT, plane_smem(g), g->stream, 
         g->dev, Wf, mode, param, inverse);
   });
   PWB_LAUNCH_CHECK();
@@ -445,11 +453,11 @@ int launch_full_to_natural(pwb_grid* g, int nvec, const double2* Wf, int mode, d
   dim3 grid(tiles(g), nvec);
   if (out_c)
     pencil_variant(g, [&](auto fx) {
-    k_pencil<0, 1, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    (void)launch_k(k_pencil<0, 1, decltype(fx)>, grid, NT, pencil_smem(g), g->stream, g->dev, a);
   });
   else
     pencil_variant(g, [&](auto fx) {
-    k_pencil<0, 2, decltype(fx)><<<grid, NT, pencil_smem(g), g->stream>>>(g->dev, a);
+    (void)launch_k(k_pencil<0, 2, decltype(fx)>, grid, NT, pencil_smem(g), g->stream, g->dev, a);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;

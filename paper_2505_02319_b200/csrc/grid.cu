@@ -12,6 +12,7 @@
 namespace pwb {
 
 unsigned long long g_launches = 0;
+bool g_pdl = getenv("PWB_NO_PDL") == nullptr;
 static thread_local std::string t_err;
 void set_error(const std::string& msg) { t_err = msg; }
 const char* last_error() { return t_err.c_str(); }

@@ -5,6 +5,7 @@
 // split of a Dyson solve; off by default (zero overhead: one branch).
 #pragma once
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -32,6 +33,11 @@ struct Profiler {
   double ms[PROF_NCAT] = {0};
   long long count[PROF_NCAT] = {0};
   long long units[PROF_NCAT] = {0};
+  // per category, histogram over floor(log2(units)) (live rows of the launch group)
+  static constexpr int NB = 16;
+  double hms[PROF_NCAT][NB] = {};
+  long long hcnt[PROF_NCAT][NB] = {};
+  int rows_hint = 0;   // live rows of the running CG iteration (0 = unknown)
 
   cudaEvent_t take() {
     if (pool.empty()) {
@@ -63,6 +69,9 @@ struct Profiler {
         ms[p.cat] += t;
         count[p.cat] += 1;
         units[p.cat] += p.units;
+        const int bkt = p.units > 0 ? std::min(NB - 1, 63 - __builtin_clzll((unsigned long long)p.units)) : 0;
+        hms[p.cat][bkt] += t;
+        hcnt[p.cat][bkt] += 1;
       }
       pool.push_back(p.a);
       pool.push_back(p.b);
@@ -75,6 +84,10 @@ struct Profiler {
       ms[i] = 0;
       count[i] = 0;
       units[i] = 0;
+      for (int b = 0; b < NB; ++b) {
+        hms[i][b] = 0;
+        hcnt[i][b] = 0;
+      }
     }
   }
 };

@@ -22,7 +22,8 @@
 // m-fragments (warp-uniform predicates), so ragged N_occ per k (31..35 at
 // BASELINE configs[1]) does not pay for 64-wide blocks.
 //
-// Complex products are four real DMMAs (re.re, im.im, re.im, im.re).
+// Complex products use three real DMMAs (Gauss: t1 = a.re b.re, t2 = a.im b.im,
+// t3 = (a.re +- a.im)(b.re + b.im)); the combination is formed once per output.
 // Measured on B200: DMMA 37.1 TFLOP/s, DFMA 34.0 TFLOP/s (tools/fp64_peak.cu).
 #include <cstring>
 
@@ -31,17 +32,16 @@
 namespace pwb {
 
 constexpr int TR = kProjTileRows;   // rows per tile (<= 2 DMMA n-fragments)
-constexpr int KC = 64;              // sphere coefficients per pipeline chunk
+constexpr int KC = kProjChunk;      // sphere coefficients per pipeline chunk
 constexpr int MF = 5;               // m fragments per block
 constexpr int CM = 8 * MF;          // orbitals per block
 constexpr int NW = 8;               // warps per CTA
 constexpr int SC = 3;               // pipeline stages
-constexpr int RSC = KC + 4;         // coef smem row stride (double2): 64 B mod 128 B
-constexpr int RSP = KC + 2;         // apply Phi row stride: 32 B mod 128 B
+constexpr int RSC = kProjRowStride; // smem / chunk-major row stride (double2): 64 B mod 128 B
 constexpr int RSX = KC + 4;         // apply X row stride
 constexpr int RSM = CM + 4;         // apply C row stride (44 = 4 mod 8)
 constexpr int kCoefStage = (TR + CM) * RSC;              // double2 per coef stage
-constexpr int kApplyStage = CM * RSP + TR * RSX + TR * RSM;
+constexpr int kApplyStage = CM * RSC + TR * RSX + TR * RSM;
 constexpr size_t kCoefSmem = (size_t)SC * kCoefStage * 16 + (size_t)(NW / 2) * CM * TR * 16 + 64;
 constexpr size_t kApplySmem = (size_t)SC * kApplyStage * 16 + 64;
 static_assert(kCoefSmem <= 232448 && kApplySmem <= 232448, "stage ring exceeds 227 KB");
@@ -178,35 +178,40 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(NW * 32) : "memory");
 }
 
+// chunk-major Phi block: orbitals m0 .. m0 + nm - 1 of chunk c of block k
+__device__ __forceinline__ const double2* phic_at(const ProjArgs& a, int k, int nocc, int c,
+                                                  int m0) {
+  return a.phic + a.phic_off[k] + ((size_t)c * nocc + m0) * RSC;
+}
+
 // Producer warp (warp NW) of the coef kernel: walks the same (item, chunk)
 // sequence as the consumers and keeps SC stages in flight; lane l copies X
-// row l and Phi rows l and l + 32 of the current item (sources resolved once
-// per item, so the row-list lookups are off the per-chunk path).
+// row l, lane 31 the chunk's Phi block (one contiguous bulk copy of the
+// chunk-major layout).  Sources are resolved once per item.
 __device__ void coef_producer(const ProjArgs& a, const CoefGeom& g, const double2* X,
                               double2* stages, uint64_t* full, uint64_t* empty, int lane) {
   CoefCursor c;
   c.first(a, g);
-  int cur = -1;
-  const double2 *xs = nullptr, *p0 = nullptr, *p1 = nullptr;
+  int cur = -1, nocc = 0;
+  const double2* xs = nullptr;
   uint32_t bytes = 0;
   for (unsigned n = 0; c.valid; ++n) {
     const int s = n % SC;
     if (n >= SC) mbar_wait(&empty[s], ((n / SC) + 1) & 1);
     if (c.item != cur) {
       cur = c.item;
-      const double2* phi = a.phi + ((size_t)a.off[c.it.t.k] + c.it.m0) * a.nbp;
+      nocc = a.nocc[c.it.t.k];
       xs = lane < c.it.t.nrows ? X + (size_t)xrow(a, c.it.t, lane) * a.nbp : nullptr;
-      p0 = lane < c.it.nm ? phi + (size_t)lane * a.nbp : nullptr;
-      p1 = lane + 32 < c.it.nm ? phi + (size_t)(lane + 32) * a.nbp : nullptr;
-      bytes = (uint32_t)(c.it.t.nrows + c.it.nm) * KC * 16;
+      bytes = (uint32_t)c.it.t.nrows * KC * 16 + (uint32_t)c.it.nm * RSC * 16;
     }
     const size_t g0 = (size_t)c.chunk * KC;
     double2* buf = stages + s * kCoefStage;
     if (lane == 0) mbar_expect_tx(&full[s], bytes);
     __syncwarp();
     if (xs) bulk_g2s(buf + lane * RSC, xs + g0, KC * 16, &full[s]);
-    if (p0) bulk_g2s(buf + (TR + lane) * RSC, p0 + g0, KC * 16, &full[s]);
-    if (p1) bulk_g2s(buf + (TR + lane + 32) * RSC, p1 + g0, KC * 16, &full[s]);
+    if (lane == 31)
+      bulk_g2s(buf + TR * RSC, phic_at(a, c.it.t.k, nocc, c.chunk, c.it.m0),
+               (uint32_t)c.it.nm * RSC * 16, &full[s]);
     c.next(a, g);
   }
 }
@@ -215,6 +220,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     k_proj_coef(ProjArgs a, const double2* __restrict__ X, int nt_host, int tile_cap, int mtiles,
                 int smax, double2* __restrict__ part, double2* __restrict__ C,
                 unsigned* __restrict__ counters) {
+  pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
   double2* stages = sm;
   double2* red = sm + SC * kCoefStage;   // [NW/2][CM][TR]
@@ -239,7 +245,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   }
   CoefCursor cons;
   cons.first(a, g);
-  double cr[MF][2][2], ci[MF][2][2];
+  // 3-multiplication complex product: t1 = sum pr xr, t2 = sum pi xi,
+  // t3 = sum (pr - pi)(xr + xi);  Re = t1 + t2, Im = t3 - t1 + t2
+  double t1[MF][2][2], t2[MF][2][2], t3[MF][2][2];
   unsigned seq = 0;
   while (cons.valid) {
     const CoefItem& it = cons.it;
@@ -248,8 +256,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
       for (int ma = 0; ma < MF; ++ma)
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb) {
-          cr[ma][nb][0] = cr[ma][nb][1] = 0.0;
-          ci[ma][nb][0] = ci[ma][nb][1] = 0.0;
+          t1[ma][nb][0] = t1[ma][nb][1] = 0.0;
+          t2[ma][nb][0] = t2[ma][nb][1] = 0.0;
+          t3[ma][nb][0] = t3[ma][nb][1] = 0.0;
         }
     }
     const int s = seq % SC;
@@ -260,32 +269,25 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
     for (int kk = 0; kk < KC / (4 * NW); ++kk) {
       const int gl = 4 * (w + NW * kk) + c4;
-      double2 av[MF], bv[2];
+      double2 bv[2];
+      double bs[2];
 #pragma unroll
-      for (int ma = 0; ma < MF; ++ma)
-        av[ma] = ma < nfm ? ps[(8 * ma + r4) * RSC + gl] : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb)
+      for (int nb = 0; nb < 2; ++nb) {
         bv[nb] = nb < nfn ? xs[(8 * nb + r4) * RSC + gl] : make_double2(0.0, 0.0);
-      // conj(phi) * x : re = pr xr + pi xi ; im = pr xi - pi xr
-#pragma unroll
-      for (int ma = 0; ma < MF; ++ma) {
-        if (ma >= nfm) break;
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb) {
-          if (nb >= nfn) break;
-          dmma(cr[ma][nb][0], cr[ma][nb][1], av[ma].x, bv[nb].x);
-          dmma(ci[ma][nb][0], ci[ma][nb][1], av[ma].x, bv[nb].y);
-        }
+        bs[nb] = bv[nb].x + bv[nb].y;
       }
+      // conj(phi) * x : re = pr xr + pi xi ; im = pr xi - pi xr  (3 real products)
 #pragma unroll
       for (int ma = 0; ma < MF; ++ma) {
         if (ma >= nfm) break;
+        const double2 av = ps[(8 * ma + r4) * RSC + gl];
+        const double ad = av.x - av.y;
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb) {
           if (nb >= nfn) break;
-          dmma(cr[ma][nb][0], cr[ma][nb][1], av[ma].y, bv[nb].y);
-          dmma(ci[ma][nb][0], ci[ma][nb][1], -av[ma].y, bv[nb].x);
+          dmma(t1[ma][nb][0], t1[ma][nb][1], av.x, bv[nb].x);
+          dmma(t2[ma][nb][0], t2[ma][nb][1], av.y, bv[nb].y);
+          dmma(t3[ma][nb][0], t3[ma][nb][1], ad, bs[nb]);
         }
       }
     }
@@ -303,7 +305,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
               red[((w - NW / 2) * CM + 8 * ma + r4) * TR + 8 * nb + 2 * c4 + h] =
-                  make_double2(cr[ma][nb][h], ci[ma][nb][h]);
+                  make_double2(t1[ma][nb][h] + t2[ma][nb][h],
+                               t3[ma][nb][h] - t1[ma][nb][h] + t2[ma][nb][h]);
       }
       consumer_sync();
       if (w < NW / 2) {
@@ -314,7 +317,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               double2& slot = red[(w * CM + 8 * ma + r4) * TR + 8 * nb + 2 * c4 + h];
-              slot = make_double2(cr[ma][nb][h] + slot.x, ci[ma][nb][h] + slot.y);
+              slot = make_double2(t1[ma][nb][h] + t2[ma][nb][h] + slot.x,
+                                  t3[ma][nb][h] - t1[ma][nb][h] + t2[ma][nb][h] + slot.y);
             }
       }
       consumer_sync();
@@ -342,22 +346,37 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         }
         consumer_sync();
         if (last) {
+          // Sum the splits of the valid entries in fixed order.  The splits are cut
+          // into G contiguous groups summed by different threads (all loads of a
+          // group batch in flight together), then the groups are added in order:
+          // a handful of L2 round trips instead of one per 8 splits per entry.
           __threadfence();
           const double2* p0 = part + tile_id * (CM * TR);
-          for (int i = threadIdx.x; i < CM * TR; i += NW * 32) {
-            const int m = i / TR, r = i - m * TR;
-            if (r >= done.t.nrows || m >= done.nm) continue;
-            double2 v = __ldcg(&p0[i]);
-            int q = 1;
-            // loads issued 8 at a time (serialised on L2 latency otherwise), summed in order
-            for (; q + 8 <= g.nsplit; q += 8) {
+          const int nr = done.t.nrows;
+          const int E = nr * done.nm;   // entry e -> (m = e / nr, r = e % nr)
+          const int G = min(NW / 2, (g.nsplit + 7) / 8);
+          const int L = (g.nsplit + G - 1) / G;
+          for (int j = threadIdx.x; j < G * E; j += NW * 32) {
+            const int q = j / E, e = j - q * E;
+            const int m = e / nr, i = m * TR + (e - m * nr);
+            const int s1 = min(g.nsplit, (q + 1) * L);
+            double2 v = make_double2(0.0, 0.0);
+            for (int sb = q * L; sb < s1; sb += 8) {
               double2 u[8];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) u[j] = __ldcg(&p0[(size_t)(q + j) * stride + i]);
+              for (int t = 0; t < 8; ++t)
+                u[t] = sb + t < s1 ? __ldcg(&p0[(size_t)(sb + t) * stride + i])
+                                   : make_double2(0.0, 0.0);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v = cadd(v, u[j]);
+              for (int t = 0; t < 8; ++t) v = cadd(v, u[t]);
             }
-            for (; q < g.nsplit; ++q) v = cadd(v, __ldcg(&p0[(size_t)q * stride + i]));
+            red[q * (CM * TR) + i] = v;
+          }
+          consumer_sync();
+          for (int e = threadIdx.x; e < E; e += NW * 32) {
+            const int m = e / nr, r = e - m * nr, i = m * TR + r;
+            double2 v = red[i];
+            for (int q = 1; q < G; ++q) v = cadd(v, red[q * (CM * TR) + i]);
             C[(size_t)(done.t.row0 + r) * a.ldc + done.m0 + m] = v;
           }
           if (threadIdx.x == 0) counters[tile_id] = 0u;
@@ -401,8 +420,8 @@ struct ApplyCursor {
   }
 };
 
-// Producer warp of the apply kernel: lane l copies Phi rows l, l + 32 of the
-// m block, and (l < 16) X row l of the chunk, (16 <= l < 32) C row l - 16.
+// Producer warp of the apply kernel: lane 31 copies the chunk's Phi block (one
+// contiguous bulk copy), lane l < 16 X row l of the chunk, 16 <= l < 32 C row l - 16.
 __device__ void apply_producer(const ProjArgs& a, const double2* C, const double2* Xin,
                                bool want_x, int ntiles, double2* stages, uint64_t* full,
                                uint64_t* empty, int lane) {
@@ -414,18 +433,17 @@ __device__ void apply_producer(const ProjArgs& a, const double2* C, const double
     const int nr = c.t.nrows;
     const int m0 = c.mblk * CM, nm = min(CM, c.nocc - m0);
     const bool with_x = want_x && c.mblk == c.nmb - 1;
-    const size_t g0 = (size_t)(c.item % c.nchunk) * KC;
-    const uint32_t bytes = (uint32_t)nm * KC * 16 + (with_x ? (uint32_t)nr * KC * 16 : 0u) +
+    const int chunk = c.item % c.nchunk;
+    const size_t g0 = (size_t)chunk * KC;
+    const uint32_t bytes = (uint32_t)nm * RSC * 16 + (with_x ? (uint32_t)nr * KC * 16 : 0u) +
                            (uint32_t)nr * nm * 16;
     double2* ps = stages + s * kApplyStage;
-    double2* xs = ps + CM * RSP;
+    double2* xs = ps + CM * RSC;
     double2* cs = xs + TR * RSX;
     if (lane == 0) mbar_expect_tx(&full[s], bytes);
     __syncwarp();
-    const double2* phi = a.phi + ((size_t)a.off[c.t.k] + m0) * a.nbp + g0;
-    if (lane < nm) bulk_g2s(ps + lane * RSP, phi + (size_t)lane * a.nbp, KC * 16, &full[s]);
-    if (lane + 32 < nm)
-      bulk_g2s(ps + (lane + 32) * RSP, phi + (size_t)(lane + 32) * a.nbp, KC * 16, &full[s]);
+    if (lane == 31)
+      bulk_g2s(ps, phic_at(a, c.t.k, c.nocc, chunk, m0), (uint32_t)nm * RSC * 16, &full[s]);
     if (lane < TR) {
       if (with_x && lane < nr)
         bulk_g2s(xs + lane * RSX, Xin + (size_t)xrow(a, c.t, lane) * a.nbp + g0, KC * 16,
@@ -442,6 +460,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     k_proj_apply(ProjArgs a, const double2* __restrict__ C, const double2* __restrict__ Xin,
                  double2* __restrict__ Y, double ca, double cb, const int* __restrict__ active,
                  int band_mod, int nt_host) {
+  pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + SC * kApplyStage);
   uint64_t* empty = full + SC;
@@ -463,20 +482,27 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   }
   ApplyCursor cons;
   cons.first(a, ntiles);
-  double dr[2][2], di[2][2];
+  // 3-multiplication complex product: t1 = sum cr pr, t2 = sum ci pi,
+  // t3 = sum (cr + ci)(pr + pi);  Re = t1 - t2, Im = t3 - t1 - t2
+  double t1[2][2], t2[2][2], t3[2][2];
   unsigned seq = 0;
   while (cons.valid) {
     if (cons.mblk == 0) {
-      dr[0][0] = dr[0][1] = dr[1][0] = dr[1][1] = 0.0;
-      di[0][0] = di[0][1] = di[1][0] = di[1][1] = 0.0;
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb) {
+        t1[jb][0] = t1[jb][1] = 0.0;
+        t2[jb][0] = t2[jb][1] = 0.0;
+        t3[jb][0] = t3[jb][1] = 0.0;
+      }
     }
     const int s = seq % SC;
     mbar_wait(&full[s], (seq / SC) & 1);
     const double2* ps = sm + s * kApplyStage;
-    const double2* xs = ps + CM * RSP;
+    const double2* xs = ps + CM * RSC;
     const double2* cs = xs + TR * RSX;
     const int nm = min(CM, cons.nocc - cons.mblk * CM);
     const int nfn = (cons.t.nrows + 7) >> 3;
+#pragma unroll 2
     for (int ms = 0; ms < nm; ms += 4) {
       const int m = ms + c4;
       const bool mok = m < nm;   // contraction index: padding must be exactly zero
@@ -484,19 +510,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
       for (int jb = 0; jb < 2; ++jb)   // A[j = r4][k = c4] = C[row j][m]
         av[jb] = (mok && jb < nfn) ? cs[(8 * jb + r4) * RSM + m] : make_double2(0.0, 0.0);
-      const double2 bv = mok ? ps[m * RSP + 8 * w + r4] : make_double2(0.0, 0.0);   // Phi[m][g]
-      // C * Phi : re = cr pr - ci pi ; im = cr pi + ci pr
+      const double2 bv = mok ? ps[m * RSC + 8 * w + r4] : make_double2(0.0, 0.0);   // Phi[m][g]
+      const double bs = bv.x + bv.y;
+      // C * Phi : re = cr pr - ci pi ; im = cr pi + ci pr  (3 real products)
 #pragma unroll
       for (int jb = 0; jb < 2; ++jb) {
         if (jb >= nfn) break;
-        dmma(dr[jb][0], dr[jb][1], av[jb].x, bv.x);
-        dmma(di[jb][0], di[jb][1], av[jb].x, bv.y);
-      }
-#pragma unroll
-      for (int jb = 0; jb < 2; ++jb) {
-        if (jb >= nfn) break;
-        dmma(dr[jb][0], dr[jb][1], -av[jb].y, bv.y);
-        dmma(di[jb][0], di[jb][1], av[jb].y, bv.x);
+        dmma(t1[jb][0], t1[jb][1], av[jb].x, bv.x);
+        dmma(t2[jb][0], t2[jb][1], av[jb].y, bv.y);
+        dmma(t3[jb][0], t3[jb][1], av[jb].x + av[jb].y, bs);
       }
     }
     if (cons.mblk == cons.nmb - 1) {   // epilogue: D fragment row j = r4, g = 2 c4 + {0,1}
@@ -511,8 +533,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         for (int h = 0; h < 2; ++h) {
           const int gl = 8 * w + 2 * c4 + h;
           const double2 x = want_x ? xs[r * RSX + gl] : make_double2(0.0, 0.0);
-          Y[(size_t)row * a.nbp + g0 + gl] =
-              make_double2(ca * x.x + cb * dr[jb][h], ca * x.y + cb * di[jb][h]);
+          const double dr = t1[jb][h] - t2[jb][h];
+          const double di = t3[jb][h] - t1[jb][h] - t2[jb][h];
+          Y[(size_t)row * a.nbp + g0 + gl] = make_double2(ca * x.x + cb * dr, ca * x.y + cb * di);
         }
       }
     }
@@ -522,6 +545,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     cons.next(a);
   }
 }
+
 
 // ---------------------------------------------------------------------------
 static int proj_configure() {
@@ -608,7 +632,7 @@ int proj_coeffs(const ProjPlan& pl, ProjArgs a, const double2* X, double2* part,
   a.nrows_total = pl.nrows;
   const long items = (long)cap * pl.mtiles * pl.nsplit;
   const int grid = (int)std::min<long>(items, kSM);
-  k_proj_coef<<<grid, (NW + 1) * 32, kCoefSmem, st>>>(a, X, (int)pl.tiles.size(), cap, pl.mtiles,
+  (void)launch_k(k_proj_coef, grid, (NW + 1) * 32, kCoefSmem, st, a, X, (int)pl.tiles.size(), cap, pl.mtiles,
                                                 pl.nsplit, part, C,
                                                 reinterpret_cast<unsigned*>(pl.counters.ptr));
   PWB_LAUNCH_CHECK();
@@ -623,10 +647,58 @@ int proj_apply(const ProjPlan& pl, ProjArgs a, const double2* C, const double2* 
   a.nrows_total = pl.nrows;
   const long items = (long)cap * (a.nbp / KC);
   const int grid = (int)std::min<long>(items, kSM);
-  k_proj_apply<<<grid, (NW + 1) * 32, kApplySmem, st>>>(a, C, Xin, Y, ca, cb, active,
+  (void)launch_k(k_proj_apply, grid, (NW + 1) * 32, kApplySmem, st, a, C, Xin, Y, ca, cb, active,
                                                   band_mod > 0 ? band_mod : 1,
                                                   (int)pl.tiles.size());
   PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// chunk-major copy of the orbital rows (one CTA per (orbital row, chunk))
+__global__ void k_phi_chunk(const double2* __restrict__ phi, int nbp, int nk,
+                            const int* __restrict__ off, const int* __restrict__ nocc,
+                            const int* __restrict__ phic_off, double2* __restrict__ phic) {
+  pdl_wait();
+  const int b = blockIdx.x, c = blockIdx.y;
+  int k = 0;
+  while (k + 1 < nk && off[k + 1] <= b) ++k;
+  const int m = b - off[k];
+  double2* dst = phic + phic_off[k] + ((size_t)c * nocc[k] + m) * RSC;
+  for (int i = threadIdx.x; i < RSC; i += blockDim.x)
+    dst[i] = i < KC ? phi[(size_t)b * nbp + (size_t)c * KC + i] : make_double2(0.0, 0.0);
+}
+
+int proj_chunked(const double2* phi, int nbp, const std::vector<int>& off_host,
+                 const std::vector<int>& nocc_host, DevBuf& phic, DevBuf& d_phic_off,
+                 cudaStream_t st) {
+  if (nbp % KC) return fail(PWB_ERR_UNSUPPORTED, "projector: row stride not a multiple of 64");
+  const int nk = (int)nocc_host.size(), nchunk = nbp / KC;
+  std::vector<int> po(nk), meta(3 * nk);
+  long long tot = 0;
+  int nband = 0;
+  for (int k = 0; k < nk; ++k) {
+    po[k] = (int)tot;
+    tot += (long long)nchunk * nocc_host[k] * RSC;
+    nband += nocc_host[k];
+  }
+  if (tot > 0x7fffffffLL) return fail(PWB_ERR_UNSUPPORTED, "chunk-major orbitals exceed 2^31");
+  for (int k = 0; k < nk; ++k) {
+    meta[k] = off_host[k];
+    meta[nk + k] = nocc_host[k];
+    meta[2 * nk + k] = po[k];
+  }
+  PWB_TRY(phic.ensure((size_t)std::max<long long>(tot, 1) * sizeof(double2)));
+  PWB_TRY(d_phic_off.ensure(3 * (size_t)nk * sizeof(int)));
+  PWB_CUDA(cudaMemcpyAsync(d_phic_off.ptr, meta.data(), meta.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, st));
+  const int* dm = as<int>(d_phic_off);
+  if (nband > 0) {
+    (void)launch_k(k_phi_chunk, dim3(nband, nchunk), 64, 0, st, phi, nbp, nk, dm, dm + nk,
+                   dm + 2 * nk, as<double2>(phic));
+    PWB_LAUNCH_CHECK();
+  }
+  PWB_CUDA(cudaStreamSynchronize(st));   // meta is a host temporary
   return PWB_OK;
 }
 

@@ -9,6 +9,8 @@
 namespace pwb {
 
 constexpr int kProjTileRows = 16;   // rows per projector tile (<= 2 DMMA n-fragments)
+constexpr int kProjChunk = 64;      // sphere coefficients per pipeline chunk
+constexpr int kProjRowStride = kProjChunk + 4;   // padded smem / chunk-major row (double2)
 
 struct ProjTile {
   int row0;   // first row of X in this tile
@@ -26,7 +28,20 @@ struct ProjArgs {
   int nrows_total;
   const int* rows;      // optional: compact row i -> X row rows[i] (active-row compaction)
   const int* ntiles;    // optional device tile count: CTAs with blockIdx.x >= *ntiles exit
+  // chunk-major copy of phi: block k, chunk c, orbital m at
+  // phic + phic_off[k] + (c * nocc[k] + m) * kProjRowStride (pads zero), so the
+  // orbitals of one chunk are ONE contiguous TMA bulk copy
+  const double2* phic;
+  const int* phic_off;  // [nk], in double2
 };
+
+// Build the chunk-major copy of the orbital rows phi [nband][nbp] (k blocks at
+// off_host[k], nocc_host[k] rows each): allocates phic, writes [off | nocc |
+// phic_off] (3 nk ints) to d_phic_off -- ProjArgs::phic_off is its base + 2 nk --
+// and runs the copy on `st` (synchronised before returning).
+int proj_chunked(const double2* phi, int nbp, const std::vector<int>& off_host,
+                 const std::vector<int>& nocc_host, DevBuf& phic, DevBuf& d_phic_off,
+                 cudaStream_t st);
 
 struct ProjPlan {
   std::vector<ProjTile> tiles;

@@ -27,6 +27,7 @@ __global__ void k_chi0_eps(int r0, int nrows, int ldc, const int* __restrict__ b
                            const int* __restrict__ off, const double2* __restrict__ C,
                            const double* __restrict__ coef, double* __restrict__ deps,
                            double* __restrict__ fsum) {
+  pdl_wait();
   // coef layout per band: [0] w*2f/sqrt(Omega), [1] w*f', [2] f', [3] w
   __shared__ double red[256];
   double acc = 0.0;
@@ -53,6 +54,7 @@ __global__ void k_chi0_occ(int r0, int nrows, int ldc, const int* __restrict__ b
                            const double* __restrict__ deps, const double* __restrict__ wt,
                            const double2* __restrict__ C, double2* __restrict__ Cw,
                            double* __restrict__ c2, double* __restrict__ c1) {
+  pdl_wait();
   const int i = blockIdx.x;
   const int band = r0 + i;
   const double def = (fabs(den) > thresh) ? fsum[0] / den : 0.0;
@@ -147,6 +149,8 @@ int pwb_state_create(pwb_grid* g, const int* nocc_per_k, const double* kweight,
   PWB_CUDA(cudaMemcpy(st->d_off.ptr, st->off.data(), g->nk * sizeof(int), cudaMemcpyHostToDevice));
   PWB_CUDA(cudaMemcpy(st->d_nocc.ptr, st->nocc.data(), g->nk * sizeof(int), cudaMemcpyHostToDevice));
   PWB_CUDA(cudaMemcpy(st->d_band_k.ptr, st->band_k.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
+  PWB_TRY(proj_chunked(as<double2>(st->phi), g->nbp, st->off, st->nocc, st->phic, st->phic_meta,
+                       nullptr));
 
   // per-band coefficients [w*2f/sqrt(Omega), w*f', f', w]
   std::vector<double> coef(4 * (size_t)nb);
@@ -280,7 +284,7 @@ int pwb_chi0_begin(pwb_state* st, int b0, int b1, const double* dv, double* fsum
   CgBatch& cg = st->cg;
   PWB_TRY(proj_coeffs(cg.plan1, a, dvpsi, as<double2>(cg.part), as<double2>(st->cm), s));
   double* deps = as<double>(st->scal);
-  k_chi0_eps<<<1, 256, 0, s>>>(b0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_off),
+  (void)launch_k(k_chi0_eps, 1, 256, 0, s, b0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_off),
                                as<double2>(st->cm), as<double>(st->d_coef), deps, fsum);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -302,7 +306,7 @@ int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, d
   double* c2 = deps + n;
   double* c1 = deps + 2 * n;
   ProjArgs a = proj_args(st);
-  k_chi0_occ<<<n, 64, 0, s>>>(b0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_nocc),
+  (void)launch_k(k_chi0_occ, n, 64, 0, s, b0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_nocc),
                               as<double>(st->d_coef), fsum, st->fp_den, st->fp_thresh, deps,
                               as<double>(st->wt), as<double2>(st->cm), as<double2>(st->cw), c2,
                               c1);
@@ -417,7 +421,11 @@ int pwb_project_generic(int nb, int nocc, const double* phi, int ncol, double* x
     P = as<double2>(pphi);
     XP = as<double2>(px);
   }
+  static thread_local DevBuf gphic, gmeta;
+  PWB_TRY(proj_chunked(P, nbp, std::vector<int>{0}, std::vector<int>{nocc}, gphic, gmeta, nullptr));
   ProjArgs a;
+  a.phic = as<double2>(gphic);
+  a.phic_off = as<int>(gmeta) + 2;
   a.phi = P;
   a.off = as<int>(meta);
   a.nocc = as<int>(meta) + 1;
@@ -469,7 +477,7 @@ int pwb_chi0_parts(pwb_state* st, const double* dv, double* diag_host, double* d
   }
   if (dphi) {
     double* deps = as<double>(st->scal);
-    k_chi0_occ<<<n, 64, 0, s>>>(0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_nocc),
+    (void)launch_k(k_chi0_occ, n, 64, 0, s, 0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_nocc),
                                 as<double>(st->d_coef), as<double>(st->fsum), st->fp_den,
                                 st->fp_thresh, deps, as<double>(st->wt), as<double2>(st->cm),
                                 as<double2>(st->cw), deps + n, deps + 2 * n);
@@ -526,6 +534,16 @@ int pwb_profile_read(double* ms, long long* count, long long* units) {
     count[i] = pwb::prof().count[i];
     units[i] = pwb::prof().units[i];
   }
+  return PWB_OK;
+}
+int pwb_profile_hist(double* ms, long long* count) {
+  cudaDeviceSynchronize();
+  pwb::prof().flush();
+  for (int i = 0; i < pwb::PROF_NCAT; ++i)
+    for (int b = 0; b < pwb::Profiler::NB; ++b) {
+      ms[i * pwb::Profiler::NB + b] = pwb::prof().hms[i][b];
+      count[i * pwb::Profiler::NB + b] = pwb::prof().hcnt[i][b];
+    }
   return PWB_OK;
 }
 }  // extern "C"

@@ -81,6 +81,7 @@ struct pwb_state {
   double fp_thresh = 0.0;    // 1e-14 * sum_k w_k nocc_k
   pwb::DevBuf phi, d_off, d_nocc, d_band_k, d_eps, d_pshift, d_coef, vloc, rho, wt;
   pwb::DevBuf vloct;         // x-major V_local for the fused pencil multiply
+  pwb::DevBuf phic, phic_meta;   // chunk-major orbitals for the projector (proj.cuh)
   pwb::DevBuf psir;          // psi(r) cache for rows [shard_b0, shard_b1)
   int psir_b0 = -1, psir_b1 = -1;
   // chi0 workspaces

@@ -15,6 +15,7 @@ constexpr int kDotBlocks = 148;
 __global__ void __launch_bounds__(NTV) k_dot_partial(int n, const double* __restrict__ x,
                                                      const double* __restrict__ y,
                                                      double* __restrict__ part) {
+  pdl_wait();
   __shared__ double red[NTV];
   double s = 0.0;
   for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV) s += x[i] * y[i];
@@ -30,6 +31,7 @@ __global__ void __launch_bounds__(NTV) k_dot_partial(int n, const double* __rest
 // out[0] = sum(part) (+= when accumulate), optional sqrt
 __global__ void k_dot_final(int np, const double* __restrict__ part, double* __restrict__ out,
                             int accumulate, int take_sqrt) {
+  pdl_wait();
   __shared__ double red[NTV];
   double s = 0.0;
   for (int i = threadIdx.x; i < np; i += NTV) s += part[i];
@@ -49,17 +51,20 @@ __global__ void k_dot_final(int np, const double* __restrict__ part, double* __r
 // y -= c[0] * x   (c on device; sign flips via neg)
 __global__ void k_axpy_dev(int n, const double* __restrict__ c, const double* __restrict__ x,
                            double* __restrict__ y) {
+  pdl_wait();
   const double a = c[0];
   for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV) y[i] -= a * x[i];
 }
 
 __global__ void k_axpy_host(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_wait();
   for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV) y[i] += a * x[i];
 }
 
 // v = w / h (or 0 when h == 0: lucky breakdown, igmres.py:99-102)
 __global__ void k_normalise(int n, const double* __restrict__ h, const double* __restrict__ w,
                             double* __restrict__ v) {
+  pdl_wait();
   const double d = h[0];
   for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV)
     v[i] = d > 0.0 ? w[i] / d : 0.0;
@@ -68,6 +73,7 @@ __global__ void k_normalise(int n, const double* __restrict__ h, const double* _
 // x = x0 + sum_j y_j V_j with the reference's sequential order
 __global__ void k_combine(int n, int m, const double* __restrict__ V, const double* __restrict__ y,
                           const double* __restrict__ x0, double* __restrict__ x) {
+  pdl_wait();
   for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV) {
     double s = x0[i];
     for (int j = 0; j < m; ++j) s = s + y[j] * V[(size_t)j * n + i];
@@ -95,9 +101,9 @@ static int dot_into(const VecCtx& c, int n, const double* x, const double* y, do
                     int accumulate, int take_sqrt) {
   PWB_TRY(c.red->ensure(kDotBlocks * sizeof(double)));
   const int nb = blocks_for(n);
-  k_dot_partial<<<nb, NTV, 0, c.stream>>>(n, x, y, as<double>(*c.red));
+  (void)launch_k(k_dot_partial, nb, NTV, 0, c.stream, n, x, y, as<double>(*c.red));
   PWB_LAUNCH_CHECK();
-  k_dot_final<<<1, NTV, 0, c.stream>>>(nb, as<double>(*c.red), out, accumulate, take_sqrt);
+  (void)launch_k(k_dot_final, 1, NTV, 0, c.stream, nb, as<double>(*c.red), out, accumulate, take_sqrt);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -113,7 +119,7 @@ int pwb_vec_dot(pwb_grid* g, int n, const double* x, const double* y, double* ou
 }
 
 int pwb_vec_axpy(pwb_grid* g, int n, double a, const double* x, double* y) {
-  k_axpy_host<<<blocks_for(n), NTV, 0, vctx(g).stream>>>(n, a, x, y);
+  (void)launch_k(k_axpy_host, blocks_for(n), NTV, 0, vctx(g).stream, n, a, x, y);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -128,12 +134,12 @@ int pwb_arnoldi_mgs(pwb_grid* g, int n, int i, double* basis, double* w, double*
     for (int j = 0; j <= i; ++j) {
       double* c = hd + pass * (i + 1) + j;
       PWB_TRY(dot_into(vctx(g), n, basis + (size_t)j * n, w, c, 0, 0));
-      k_axpy_dev<<<nb, NTV, 0, vctx(g).stream>>>(n, c, basis + (size_t)j * n, w);
+      (void)launch_k(k_axpy_dev, nb, NTV, 0, vctx(g).stream, n, c, basis + (size_t)j * n, w);
       PWB_LAUNCH_CHECK();
     }
   double* nrm = hd + 2 * (i + 1);
   PWB_TRY(dot_into(c, n, w, w, nrm, 0, 1));
-  k_normalise<<<nb, NTV, 0, c.stream>>>(n, nrm, w, basis + (size_t)(i + 1) * n);
+  (void)launch_k(k_normalise, nb, NTV, 0, c.stream, n, nrm, w, basis + (size_t)(i + 1) * n);
   PWB_LAUNCH_CHECK();
   std::vector<double> hh(2 * (i + 1) + 1);
   PWB_CUDA(cudaMemcpyAsync(hh.data(), hd, hh.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -151,7 +157,7 @@ int pwb_vec_combine(pwb_grid* g, int n, int m, const double* basis, const double
   if (m > 0)
     PWB_CUDA(cudaMemcpyAsync(c.scratch->ptr, y_host, m * sizeof(double), cudaMemcpyHostToDevice,
                              c.stream));
-  k_combine<<<blocks_for(n), NTV, 0, c.stream>>>(n, m, basis, as<double>(*c.scratch), x0, x);
+  (void)launch_k(k_combine, blocks_for(n), NTV, 0, c.stream, n, m, basis, as<double>(*c.scratch), x0, x);
   PWB_LAUNCH_CHECK();
   PWB_CUDA(cudaStreamSynchronize(c.stream));
   return PWB_OK;

@@ -56,6 +56,17 @@ def main():
         res["H"] = ms
         print(f"H apply: {ms:.3f} ms per batch of {a.bands} -> {ms / a.bands * 1e3:.2f} us/band, "
               f"{a.bands / ms * 1e3:.0f} band-applies/s, B_H model {bh * a.bands / ms / 1e6:.0f} GB/s")
+    if a.what == "qsweep":   # projector launches at CG-tail sizes (time them under ncu)
+        nbp = dg.nbp
+        phi = synth.random_orthonormal(rng, nbp, a.nocc)
+        P = torch.from_numpy(np.ascontiguousarray(phi.T)).cuda()
+        for ncol in (1, 4, 8, 16, 32, 64, 128, 256):
+            Xs = torch.randn(ncol, nbp, dtype=torch.complex128, device="cuda")
+            for _ in range(a.reps):
+                lib.pwb_project_generic(nbp, a.nocc, ptr(P), ncol, ptr(Xs))
+            torch.cuda.synchronize()
+            print("ncol", ncol, "done")
+        return
     if "q" in a.what:
         Y = X.clone()
         for _ in range(3):
