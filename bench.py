@@ -34,6 +34,9 @@ METRIC = "H*psi band-applies/s per inexact-GMRES delta_rho solve"
 UNIT = "band-applies/s"
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0
+# DRAM bytes per band-apply of the H-apply kernels from the committed ncu --set full
+# capture (profiles/r01_ncu_happly_summary.txt), for roofline.traffic
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
 
 
 def parse():
@@ -175,12 +178,23 @@ def roofline_from_profile(prof, gs):
     ms, count, units = prof["ham_apply"]
     b_h = 64.0 * n_g + 32.0 * n_b
     avg_ms = ms / max(count, 1)
-    bytes_per_launch = b_h * units / max(count, 1)
+    bands = units / max(count, 1)
+    bytes_per_launch = b_h * bands
     achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
+    traffic, traffic_src = None, None
+    try:
+        with open(TRAFFIC_FILE) as fh:
+            t = json.load(fh)["ham_apply"]
+        if n_g == 48 ** 3:   # the capture is of this grid
+            traffic = t["dram_bytes_per_band_apply"] * bands
+            traffic_src = t["capture"]
+    except (OSError, KeyError, ValueError):
+        pass
     return {
         "kernel": "ham_apply (plane_inv + pencil V(r) + plane_fwd, one batched H psi)",
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": None, "peak_source": how,
+        "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+        "peak_source": how,
         "algorithmic_bytes_per_band_apply": b_h,
         "avg_launch_ms": avg_ms, "bands_per_launch": units / max(count, 1),
         "share_of_kernel_time": {k: (v / total if total > 0 else 0.0) for k, v in shares.items()},

@@ -36,10 +36,16 @@ __global__ void __launch_bounds__(NTA) k_drho_partial(GridDev g, int nband, int 
     for (int i = threadIdx.x; i < nx * Tp; i += NTA) sm[i] = make_double2(0.0, 0.0);
     __syncthreads();
     const double2* src = W + (size_t)b * g.nxa * nyz;
-    for (int i = threadIdx.x; i < g.nxa * nt; i += NTA) {
-      const int p = i / nt, t = i - p * nt;
-      sm[g.xa[p] * Tp + t] = src[(size_t)p * nyz + t0 + t];
-    }
+    staged_copy<6, NTA>(
+        g.nxa * nt,
+        [&](int i) {
+          const int p = i / nt;
+          return __ldg(&src[(size_t)p * nyz + t0 + (i - p * nt)]);
+        },
+        [&](int i, double2 v) {
+          const int p = i / nt;
+          sm[g.xa[p] * Tp + (i - p * nt)] = v;
+        });
     __syncthreads();
     FX::template run<NTA>(g, sm, nt, Tp, 1, nullptr, true);
     const double a2 = c2[b], a1 = c1[b];

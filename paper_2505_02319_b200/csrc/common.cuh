@@ -73,6 +73,27 @@ __host__ __device__ __forceinline__ double2 cconj(double2 a) { return make_doubl
 
 constexpr int kSM = 148;   // B200 SM count (grid sizing)
 
+// Global -> smem staging with U loads in flight per thread.  A plain
+// `sm[f(i)] = src[g(i)]` loop serialises on every load's latency (the store
+// may alias the generic source pointer, so loads cannot be hoisted); ncu showed
+// long-scoreboard stalls dominating the pencil and plane passes.
+template <int U, int NTH, class Load, class Store>
+__device__ __forceinline__ void staged_copy(int n, Load load, Store store) {
+  for (int i0 = threadIdx.x; i0 < n; i0 += U * NTH) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * NTH;
+      if (i < n) v[u] = load(i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * NTH;
+      if (i < n) store(i, v[u]);
+    }
+  }
+}
+
 // --- programmatic dependent launch (PDL) ---------------------------------------
 // Kernels of the CG iteration are launched with programmatic stream
 // serialisation: the next kernel's launch and prologue overlap the tail of the

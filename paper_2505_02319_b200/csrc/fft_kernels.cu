@@ -82,10 +82,9 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_fwd(GridDev g, const
   const int ny = FY::N ? FY::N : g.ny;
   const int nyp = g.nyp;
   const double2* srcw = W + ((size_t)slot * g.nxa + p) * nyz;
-  for (int i = threadIdx.x; i < nyz; i += NT) {
-    const int z = i / ny;
-    sm[i + z * (nyp - ny)] = srcw[i];
-  }
+  staged_copy<8, NT>(
+      nyz, [&](int i) { return __ldg(&srcw[i]); },
+      [&](int i, double2 v) { sm[i + (i / ny) * (nyp - ny)] = v; });
   __syncthreads();
   FY::template run<NT>(g, sm, g.nz, 1, nyp, nullptr, false, 0);  // y lines, every z
   FZ::template run<NT>(g, sm, g.nya, nyp, 0, g.ya, false);       // z lines of active y
@@ -158,17 +157,43 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_pencil(GridDev g, PencilAr
         sm[x * Tp + t] = make_double2(0.0, 0.0);
       }
     }
-    const double2* src = a.win + (size_t)b * a.in_stride;
-    for (int i = threadIdx.x; i < a.nxin * nt; i += NT) {
-      const int p = i / nt, t = i - p * nt;
-      sm[a.xin[p] * Tp + t] = src[(size_t)p * nyz + t0 + t];
+    if (a.mode == 3) {   // stage this tile's V(r) (x-major) with the W loads: off the FFT path
+      double* smv = reinterpret_cast<double*>(sm + nx * Tp);
+      const double* vsrc = a.v + t0;
+      for (int i0 = threadIdx.x; i0 < nx * T; i0 += 8 * NT) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * NT, x = i / T, t = i - x * T;
+          v[u] = (i < nx * T && t < nt) ? __ldg(&vsrc[(size_t)x * nyz + t]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u * NT < nx * T) smv[i0 + u * NT] = v[u];
+      }
     }
+    const double2* src = a.win + (size_t)b * a.in_stride;
+    staged_copy<6, NT>(
+        a.nxin * nt,
+        [&](int i) {
+          const int p = i / nt;
+          return __ldg(&src[(size_t)p * nyz + t0 + (i - p * nt)]);
+        },
+        [&](int i, double2 v) {
+          const int p = i / nt;
+          sm[a.xin[p] * Tp + (i - p * nt)] = v;
+        });
   } else {
     const size_t base = (size_t)b * a.in_stride + (size_t)t0 * nx;
-    for (int i = threadIdx.x; i < nt * nx; i += NT) {
-      const int t = i / nx, x = i - t * nx;
-      sm[x * Tp + t] = (IN == 1) ? a.cin[base + i] : make_double2(a.rin[base + i], 0.0);
-    }
+    staged_copy<8, NT>(
+        nt * nx,
+        [&](int i) {
+          return (IN == 1) ? __ldg(&a.cin[base + i]) : make_double2(__ldg(&a.rin[base + i]), 0.0);
+        },
+        [&](int i, double2 v) {
+          const int t = i / nx;
+          sm[(i - t * nx) * Tp + t] = v;
+        });
   }
   __syncthreads();
   if (a.mode == 1) {
@@ -176,7 +201,8 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_pencil(GridDev g, PencilAr
   } else if (a.mode >= 2) {
     FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, true);
     if (a.mode == 3)   // V(r)/n_g applied inside the first pass of the forward transform
-      FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, false, -1, a.v + t0, nyz, a.vscale);
+      FX::template run<NT>(g, sm, nt, Tp, 1, nullptr, false, -1,
+                           reinterpret_cast<const double*>(sm + nx * Tp), T, a.vscale);
   }
   if (OUT == 0) {
     double2* dst = a.wout + (size_t)b * a.out_stride;
@@ -220,7 +246,9 @@ __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restric
   const int ny = FY::N ? FY::N : g.ny;
   const int nyp = g.nyp;
   double2* pl = Wf + ((size_t)v * g.nx + x) * nyz;
-  for (int i = threadIdx.x; i < nyz; i += NT) sm[i + (i / ny) * (nyp - ny)] = pl[i];
+  staged_copy<8, NT>(
+      nyz, [&](int i) { return pl[i]; },
+      [&](int i, double2 v) { sm[i + (i / ny) * (nyp - ny)] = v; });
   __syncthreads();
   if (mode == 0 && inverse) {
     FZ::template run<NT>(g, sm, g.ny, nyp, 1, nullptr, true);
@@ -248,6 +276,10 @@ __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restric
 
 size_t plane_smem(const pwb_grid* g) { return (size_t)g->nz * g->dev.nyp * sizeof(double2); }
 size_t pencil_smem(const pwb_grid* g) { return (size_t)g->nx * g->dev.tilep * sizeof(double2); }
+// W -> W pencil with the V(r) multiply: + the tile's V values (x-major doubles)
+static size_t pencil_smem_v(const pwb_grid* g) {
+  return pencil_smem(g) + (size_t)g->nx * g->dev.tile * sizeof(double);
+}
 
 static int tiles(const pwb_grid* g) { return (g->nyz + g->dev.tile - 1) / g->dev.tile; }
 
@@ -349,7 +381,7 @@ int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, doub
   a.out_stride = a.in_stride;
   dim3 grid(tiles(g), nband);
   pencil_variant(g, [&](auto fx) {
-    (void)launch_k(k_pencil<0, 0, decltype(fx)>, grid, NT, pencil_smem(g), g->stream, g->dev, a);
+    (void)launch_k(k_pencil<0, 0, decltype(fx)>, grid, NT, pencil_smem_v(g), g->stream, g->dev, a);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -465,7 +497,7 @@ int launch_full_to_natural(pwb_grid* g, int nvec, const double2* Wf, int mode, d
 
 int configure_kernels(const pwb_grid* g) {
   const size_t ps = plane_smem(g), cs = pencil_smem(g);
-  if (ps > 227 * 1024 || cs > 227 * 1024)
+  if (ps > 227 * 1024 || pencil_smem_v(g) > 227 * 1024)
     return fail(PWB_ERR_UNSUPPORTED, "grid plane does not fit in shared memory");
   cudaError_t e = cudaSuccess;
   plane_variant(g, [&](auto fy, auto fz) {
@@ -480,7 +512,8 @@ int configure_kernels(const pwb_grid* g) {
   PWB_CUDA(e);
   pencil_variant(g, [&](auto fx) {
     using FX = decltype(fx);
-    e = cudaFuncSetAttribute(k_pencil<0, 0, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+    e = cudaFuncSetAttribute(k_pencil<0, 0, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pencil_smem_v(g));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_pencil<0, 1, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
     if (e == cudaSuccess)

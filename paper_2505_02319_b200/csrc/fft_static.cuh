@@ -113,34 +113,47 @@ __device__ __forceinline__ void spass(double2* __restrict__ s, int nlines, int e
       w[r] = t;
     }
   }
+  // MR rounds of LPR lines share one load phase and one store phase (one
+  // barrier pair): fewer barriers and MR * R independent smem loads in flight
+  // for the small radices (radix-3 pass of 48 = 16 x 3 over 64 lines: 2
+  // barriers instead of 8).
+  constexpr int MR = (12 / R) > 1 ? (12 / R) : 1;
 #pragma unroll 1
-  for (int l0 = 0; l0 < nlines; l0 += LPR) {
-    const int l = l0 + l_in;
-    const bool ok = lane_ok && (l < nlines);
-    double2 v[R];
-    int base = 0;
-    if (ok) {
-      base = lbase ? lbase[l] : l * ls;
+  for (int l0 = 0; l0 < nlines; l0 += LPR * MR) {
+    double2 v[MR][R];
+    int base[MR];
+    bool ok[MR];
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = s[base + (j + r * NBF) * es];
-      if (NS == 1 && vm) {
-        // multiplier stored element-major (vm[e * vld + l]): consecutive lines are
-        // consecutive threads, so these loads coalesce
-        const double* vl = vm + l;
+    for (int m = 0; m < MR; ++m) {
+      const int l = l0 + m * LPR + l_in;
+      ok[m] = lane_ok && (l < nlines);
+      base[m] = 0;
+      if (ok[m]) {
+        base[m] = lbase ? lbase[l] : l * ls;
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          v[r] = cscale(v[r], vs * __ldg(&vl[(size_t)(j + r * NBF) * vld]));
+        for (int r = 0; r < R; ++r) v[m][r] = s[base[m] + (j + r * NBF) * es];
+        if (NS == 1 && vm) {
+          // multiplier stored element-major (vm[e * vld + l]): consecutive lines are
+          // consecutive threads, so these loads coalesce
+          const double* vl = vm + l;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            v[m][r] = cscale(v[m][r], vs * vl[(size_t)(j + r * NBF) * vld]);   // smem or global
+        }
       }
     }
     __syncthreads();
-    if (ok) {
-      if (NS > 1) {
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
+    for (int m = 0; m < MR; ++m) {
+      if (ok[m]) {
+        if (NS > 1) {
+#pragma unroll
+          for (int r = 1; r < R; ++r) v[m][r] = cmul(v[m][r], w[r]);
+        }
+        Dft<R>::run(v[m], sgn);
+#pragma unroll
+        for (int r = 0; r < R; ++r) s[base[m] + (o0 + r * NS) * es] = v[m][r];
       }
-      Dft<R>::run(v, sgn);
-#pragma unroll
-      for (int r = 0; r < R; ++r) s[base + (o0 + r * NS) * es] = v[r];
     }
     __syncthreads();
   }
