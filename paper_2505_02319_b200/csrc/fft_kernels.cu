@@ -36,10 +36,12 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_inv(GridDev g, const
   const int b = blockIdx.y;                     // plane-buffer slot
   const int row = rows ? rows[b] : b;           // sphere row (active-row compaction)
   const int k = band_k ? band_k[row] : 0;
-  const int nyz = g.nyz;
+  // plane geometry: compile-time for the codelet sizes (strides fold into addressing)
   const int ny = FY::N ? FY::N : g.ny;
-  const int nyp = g.nyp;   // odd smem row stride: conflict-free y and z lines
-  for (int i = threadIdx.x; i < g.nz * nyp; i += NT) sm[i] = make_double2(0.0, 0.0);
+  const int nz = FZ::N ? FZ::N : g.nz;
+  const int nyz = ny * nz;
+  const int nyp = FY::N ? (FY::N % 2 == 0 ? FY::N + 1 : FY::N) : g.nyp;   // odd smem stride
+  for (int i = threadIdx.x; i < nz * nyp; i += NT) sm[i] = make_double2(0.0, 0.0);
   __syncthreads();
   const int s0 = g.xr[k * (g.nxa + 1) + p];
   const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
@@ -52,8 +54,8 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_inv(GridDev g, const
     for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(src[s], scale);
   }
   __syncthreads();
-  FZ::template run<NT>(g, sm, g.nya, nyp, 0, g.ya, true);      // z lines of active y
-  FY::template run<NT>(g, sm, g.nz, 1, nyp, nullptr, true, 0);  // y lines, threads across lines
+  FZ::template run<NT>(g, sm, g.nya, nyp, 0, g.ya, true);    // z lines of active y
+  FY::template run<NT>(g, sm, nz, 1, nyp, nullptr, true, 0);  // y lines, threads across lines
   double2* dst = W + ((size_t)b * g.nxa + p) * nyz;
   for (int i = threadIdx.x; i < nyz; i += NT) {
     const int z = i / ny;
@@ -78,15 +80,16 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_fwd(GridDev g, const
   const int slot = blockIdx.y;                  // plane-buffer slot
   const int b = rows ? rows[slot] : slot;       // sphere row
   const int k = band_k ? band_k[b] : 0;
-  const int nyz = g.nyz;
   const int ny = FY::N ? FY::N : g.ny;
-  const int nyp = g.nyp;
+  const int nz = FZ::N ? FZ::N : g.nz;
+  const int nyz = ny * nz;
+  const int nyp = FY::N ? (FY::N % 2 == 0 ? FY::N + 1 : FY::N) : g.nyp;
   const double2* srcw = W + ((size_t)slot * g.nxa + p) * nyz;
   staged_copy<8, NT>(
       nyz, [&](int i) { return __ldg(&srcw[i]); },
       [&](int i, double2 v) { sm[i + (i / ny) * (nyp - ny)] = v; });
   __syncthreads();
-  FY::template run<NT>(g, sm, g.nz, 1, nyp, nullptr, false, 0);  // y lines, every z
+  FY::template run<NT>(g, sm, nz, 1, nyp, nullptr, false, 0);  // y lines, every z
   FZ::template run<NT>(g, sm, g.nya, nyp, 0, g.ya, false);       // z lines of active y
   const int s0 = g.xr[k * (g.nxa + 1) + p];
   const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
@@ -135,11 +138,16 @@ struct PencilArgs {
   const int* nact;        // optional device row count: blocks with b >= *nact exit
 };
 
-template <int IN, int OUT, class FX>
+// TC: compile-time tile (the codelet sizes' default 3072 / N), 0 = runtime g.tile;
+// with it every smem stride and index division folds to constants (ncu: integer
+// index arithmetic was half the pencil's instructions).
+template <int IN, int OUT, class FX, int TC = 0>
 __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_pencil(GridDev g, PencilArgs a) {
   pdl_wait();
   extern __shared__ double2 sm[];
-  const int T = g.tile, Tp = g.tilep, nyz = g.nyz;
+  const int T = TC ? TC : g.tile;
+  const int Tp = TC ? (TC % 2 == 0 ? TC + 1 : TC) : g.tilep;
+  const int nyz = g.nyz;
   const int nx = FX::N ? FX::N : g.nx;   // compile-time for the codelet sizes
   const int t0 = blockIdx.x * T;
   const int b = blockIdx.y;
@@ -174,14 +182,14 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_pencil(GridDev g, PencilAr
     }
     const double2* src = a.win + (size_t)b * a.in_stride;
     staged_copy<6, NT>(
-        a.nxin * nt,
+        a.nxin * T,
         [&](int i) {
-          const int p = i / nt;
-          return __ldg(&src[(size_t)p * nyz + t0 + (i - p * nt)]);
+          const int p = i / T, t = i - p * T;
+          return t < nt ? __ldg(&src[(size_t)p * nyz + t0 + t]) : make_double2(0.0, 0.0);
         },
         [&](int i, double2 v) {
-          const int p = i / nt;
-          sm[a.xin[p] * Tp + (i - p * nt)] = v;
+          const int p = i / T;
+          sm[a.xin[p] * Tp + (i - p * T)] = v;
         });
   } else {
     const size_t base = (size_t)b * a.in_stride + (size_t)t0 * nx;
@@ -206,9 +214,9 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_pencil(GridDev g, PencilAr
   }
   if (OUT == 0) {
     double2* dst = a.wout + (size_t)b * a.out_stride;
-    for (int i = threadIdx.x; i < a.nxout * nt; i += NT) {
-      const int p = i / nt, t = i - p * nt;
-      dst[(size_t)p * nyz + t0 + t] = cscale(sm[a.xout[p] * Tp + t], a.oscale);
+    for (int i = threadIdx.x; i < a.nxout * T; i += NT) {
+      const int p = i / T, t = i - p * T;
+      if (t < nt) dst[(size_t)p * nyz + t0 + t] = cscale(sm[a.xout[p] * Tp + t], a.oscale);
     }
   } else {
     const size_t base = (size_t)b * a.out_stride + (size_t)t0 * nx;
@@ -381,7 +389,12 @@ int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, doub
   a.out_stride = a.in_stride;
   dim3 grid(tiles(g), nband);
   pencil_variant(g, [&](auto fx) {
-    (void)launch_k(k_pencil<0, 0, decltype(fx)>, grid, NT, pencil_smem_v(g), g->stream, g->dev, a);
+    using FX = decltype(fx);
+    constexpr int TC = FX::N ? 3072 / FX::N : 0;
+    if (TC && g->dev.tile == TC)
+      (void)launch_k(k_pencil<0, 0, FX, TC>, grid, NT, pencil_smem_v(g), g->stream, g->dev, a);
+    else
+      (void)launch_k(k_pencil<0, 0, FX>, grid, NT, pencil_smem_v(g), g->stream, g->dev, a);
   });
   PWB_LAUNCH_CHECK();
   return PWB_OK;
@@ -514,6 +527,10 @@ int configure_kernels(const pwb_grid* g) {
     using FX = decltype(fx);
     e = cudaFuncSetAttribute(k_pencil<0, 0, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)pencil_smem_v(g));
+    constexpr int TC = FX::N ? 3072 / FX::N : 0;
+    if (e == cudaSuccess && TC)
+      e = cudaFuncSetAttribute(k_pencil<0, 0, FX, TC ? TC : 1>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pencil_smem_v(g));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_pencil<0, 1, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
     if (e == cudaSuccess)
