@@ -282,6 +282,155 @@ __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restric
   for (int i = threadIdx.x; i < nyz; i += NT) pl[i] = sm[i + (i / ny) * (nyp - ny)];
 }
 
+// ----------------------------------------------------------------------------
+// H-apply pencil for two-pass lengths N = R1 x R2 (48 = 16 x 3, 64 = 16 x 4, ...):
+// inverse x-FFT, * V(r)/n_g, forward x-FFT with 2 smem round trips instead of 6.
+//   A: W rows (active x only, zeros elsewhere) straight from global into the
+//      radix-R1 inverse pass (NS = 1) -> smem
+//   B: radix-R2 inverse pass (NS = R1, natural-order outputs x = j + r R1),
+//      * V, then the forward transform's FIRST pass in the reversed plan
+//      R2 x R1 (radix R2, NS = 1), which reads exactly those x: all in registers
+//   C: radix-R1 forward pass (NS = R2) -> the active x rows straight to global.
+// Three barriers per CTA (the generic path: about twelve).  Same twiddle table
+// and DFT codelets as the generic passes; the forward plan order differs, so
+// results agree with it to rounding, not bitwise.
+template <int N>
+struct TwoPass {
+  static constexpr bool ok = false;
+};
+template <>
+struct TwoPass<48> {   // 8 x 6: register-resident radix-16 lines spill (measured 1.63 vs 1.46 us/band)
+  static constexpr bool ok = true;
+  static constexpr int R1 = 8, R2 = 6;
+};
+template <>
+struct TwoPass<64> {
+  static constexpr bool ok = true;
+  static constexpr int R1 = 16, R2 = 4;
+};
+template <>
+struct TwoPass<96> {
+  static constexpr bool ok = true;
+  static constexpr int R1 = 16, R2 = 6;
+};
+
+template <int N>
+#ifndef PWB_PENCIL_H_MINB
+#define PWB_PENCIL_H_MINB 3   // 80-register cap; 3 CTAs/SM (smem 75 KB each)
+#endif
+__global__ void __launch_bounds__(NT, PWB_PENCIL_H_MINB) k_pencil_h(GridDev g, PencilArgs a) {
+  constexpr int R1 = TwoPass<N>::R1, R2 = TwoPass<N>::R2;
+  constexpr int TC = 3072 / N, TP = (TC % 2 == 0) ? TC + 1 : TC;
+  constexpr int NB1 = N / R1;                 // radix-R1 butterflies per line (= R2)
+  constexpr int LP1 = NT / NB1;               // lines per round, passes A and C
+  constexpr int LP2 = NT / R1;                // lines per round, pass B
+  constexpr int MB = (TC + LP2 - 1) / LP2;    // pass-B rounds held in registers
+  static_assert(NB1 == R2, "two-pass plan");
+  pdl_wait();
+  extern __shared__ double2 sm[];
+  double* smv = reinterpret_cast<double*>(sm + N * TP);   // V(r) tile, x-major [x][TC]
+  const int nyz = g.nyz;
+  const int t0 = blockIdx.x * TC;
+  const int b = blockIdx.y;
+  if (a.nact && b >= *a.nact) return;
+  const int nt = min(TC, nyz - t0);
+  const int x0 = a.xin[0], nact_x = a.nxin;   // active x: contiguous wrapped range from x0
+  const int tid = threadIdx.x;
+  // V tile (consumed in pass B; the loads overlap pass A)
+  for (int i0 = tid; i0 < N * TC; i0 += 8 * NT) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * NT, x = i / TC, t = i - x * TC;
+      v[u] = (i < N * TC && t < nt) ? __ldg(&a.v[(size_t)x * nyz + t0 + t]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u * NT < N * TC) smv[i0 + u * NT] = v[u];
+  }
+  // ---- A: inverse pass 1 (radix R1, NS = 1), inputs from global
+  {
+    const int j = tid / LP1, li = tid - j * LP1;
+    const double2* src = a.win + (size_t)b * a.in_stride;
+    if (j < NB1) {
+      for (int l = li; l < TC; l += LP1) {
+        double2 v[R1];
+#pragma unroll
+        for (int r = 0; r < R1; ++r) {
+          const int x = j + r * NB1;
+          int p = x - x0;
+          if (p < 0) p += N;
+          v[r] = (p < nact_x && l < nt) ? __ldg(&src[(size_t)p * nyz + t0 + l])
+                                        : make_double2(0.0, 0.0);
+        }
+        Dft<R1>::run(v, 1.0);
+#pragma unroll
+        for (int r = 0; r < R1; ++r) sm[(j * R1 + r) * TP + l] = v[r];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- B: inverse pass 2 (radix R2, NS = R1) -> * V -> forward pass 1 (radix R2, NS = 1)
+  {
+    const int j = tid / LP2, li = tid - j * LP2;   // j in [0, R1)
+    double2 w[R2];
+#pragma unroll
+    for (int r = 1; r < R2; ++r) {
+      const double2 t = __ldg(&g.px.tw[r * j]);   // TWS = N / (NS R) = 1
+      w[r] = make_double2(t.x, -t.y);              // inverse: conjugate
+    }
+    double2 v[MB][R2];
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      const int l = m * LP2 + li;
+      if (l < TC) {
+#pragma unroll
+        for (int r = 0; r < R2; ++r) v[m][r] = sm[(j + r * R1) * TP + l];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      const int l = m * LP2 + li;
+      if (l < TC) {
+#pragma unroll
+        for (int r = 1; r < R2; ++r) v[m][r] = cmul(v[m][r], w[r]);
+        Dft<R2>::run(v[m], 1.0);
+#pragma unroll
+        for (int r = 0; r < R2; ++r) v[m][r] = cscale(v[m][r], a.vscale * smv[(j + r * R1) * TC + l]);
+        Dft<R2>::run(v[m], -1.0);
+#pragma unroll
+        for (int r = 0; r < R2; ++r) sm[(j * R2 + r) * TP + l] = v[m][r];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- C: forward pass 2 (radix R1, NS = R2), active outputs straight to global
+  {
+    const int j = tid / LP1, li = tid - j * LP1;   // j in [0, R2)
+    if (j < NB1) {
+      double2* dst = a.wout + (size_t)b * a.out_stride;
+      for (int l = li; l < TC; l += LP1) {
+        double2 v[R1];
+#pragma unroll
+        for (int r = 0; r < R1; ++r) v[r] = sm[(j + r * R2) * TP + l];
+#pragma unroll
+        for (int r = 1; r < R1; ++r)   // twiddles (TWS = 1, forward) from L1: registers are tight
+          v[r] = cmul(v[r], __ldg(&g.px.tw[r * j]));
+        Dft<R1>::run(v, -1.0);
+        if (l < nt) {
+#pragma unroll
+          for (int r = 0; r < R1; ++r) {
+            int p = j + r * R2 - x0;
+            if (p < 0) p += N;
+            if (p < nact_x) dst[(size_t)p * nyz + t0 + l] = cscale(v[r], a.oscale);
+          }
+        }
+      }
+    }
+  }
+}
+
 size_t plane_smem(const pwb_grid* g) { return (size_t)g->nz * g->dev.nyp * sizeof(double2); }
 size_t pencil_smem(const pwb_grid* g) { return (size_t)g->nx * g->dev.tilep * sizeof(double2); }
 // W -> W pencil with the V(r) multiply: + the tile's V values (x-major doubles)
@@ -388,9 +537,16 @@ int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, doub
   a.nxout = g->nxa;
   a.out_stride = a.in_stride;
   dim3 grid(tiles(g), nband);
+  static const bool generic_only = getenv("PWB_NO_PENCIL_H") != nullptr;   // A/B measurement
   pencil_variant(g, [&](auto fx) {
     using FX = decltype(fx);
     constexpr int TC = FX::N ? 3072 / FX::N : 0;
+    if constexpr (TwoPass<FX::N>::ok) {
+      if (!generic_only && g->dev.tile == TC) {
+        (void)launch_k(k_pencil_h<FX::N>, grid, NT, pencil_smem_v(g), g->stream, g->dev, a);
+        return;
+      }
+    }
     if (TC && g->dev.tile == TC)
       (void)launch_k(k_pencil<0, 0, FX, TC>, grid, NT, pencil_smem_v(g), g->stream, g->dev, a);
     else
@@ -531,6 +687,11 @@ int configure_kernels(const pwb_grid* g) {
     if (e == cudaSuccess && TC)
       e = cudaFuncSetAttribute(k_pencil<0, 0, FX, TC ? TC : 1>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pencil_smem_v(g));
+    if constexpr (TwoPass<FX::N>::ok) {
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_pencil_h<FX::N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pencil_smem_v(g));
+    }
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_pencil<0, 1, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
     if (e == cudaSuccess)

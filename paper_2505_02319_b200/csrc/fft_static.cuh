@@ -206,7 +206,11 @@ PWB_PLAN(12, 4, 3)
 PWB_PLAN(16, 16)
 PWB_PLAN(24, 8, 3)
 PWB_PLAN(32, 8, 4)
+#ifdef PWB_PLAN48_86
+PWB_PLAN(48, 8, 6)
+#else
 PWB_PLAN(48, 16, 3)
+#endif
 PWB_PLAN(64, 16, 4)
 PWB_PLAN(96, 16, 6)
 PWB_PLAN(216, 6, 6, 6)
