@@ -7,6 +7,28 @@
 
 namespace pwb {
 
+// Two-pass plans N = R1 x R2 for the fused pencil / accumulation kernels
+// (k_pencil_h, k_drho_h): pass R1 with NS = 1, then R2 with NS = R1.
+template <int N>
+struct TwoPass {
+  static constexpr bool ok = false;
+};
+template <>
+struct TwoPass<48> {   // 8 x 6: register-resident radix-16 lines spill (measured 1.63 vs 1.46 us/band)
+  static constexpr bool ok = true;
+  static constexpr int R1 = 8, R2 = 6;
+};
+template <>
+struct TwoPass<64> {
+  static constexpr bool ok = true;
+  static constexpr int R1 = 16, R2 = 4;
+};
+template <>
+struct TwoPass<96> {
+  static constexpr bool ok = true;
+  static constexpr int R1 = 16, R2 = 6;
+};
+
 // ----------------------------------------------------------------------------
 // dispatch: compile-time codelets for the cube shapes in use, runtime engine otherwise
 #define PWB_PLANE_SHAPES(X) X(6, 6) X(8, 8) X(12, 12) X(16, 16) X(24, 24) X(32, 32) \

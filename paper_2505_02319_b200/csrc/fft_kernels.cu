@@ -218,6 +218,12 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_pencil(GridDev g, PencilAr
       const int p = i / T, t = i - p * T;
       if (t < nt) dst[(size_t)p * nyz + t0 + t] = cscale(sm[a.xout[p] * Tp + t], a.oscale);
     }
+  } else if (OUT == 3) {   // x-major complex cube [x][yz] (psi(r) cache of the accumulation)
+    double2* dst = a.cout + (size_t)b * a.out_stride;
+    for (int i = threadIdx.x; i < nx * T; i += NT) {
+      const int x = i / T, t = i - x * T;
+      if (t < nt) dst[(size_t)x * nyz + t0 + t] = cscale(sm[x * Tp + t], a.oscale);
+    }
   } else {
     const size_t base = (size_t)b * a.out_stride + (size_t)t0 * nx;
     for (int i = threadIdx.x; i < nt * nx; i += NT) {
@@ -293,27 +299,7 @@ __global__ void __launch_bounds__(NT) k_plane_full(GridDev g, double2* __restric
 //   C: radix-R1 forward pass (NS = R2) -> the active x rows straight to global.
 // Three barriers per CTA (the generic path: about twelve).  Same twiddle table
 // and DFT codelets as the generic passes; the forward plan order differs, so
-// results agree with it to rounding, not bitwise.
-template <int N>
-struct TwoPass {
-  static constexpr bool ok = false;
-};
-template <>
-struct TwoPass<48> {   // 8 x 6: register-resident radix-16 lines spill (measured 1.63 vs 1.46 us/band)
-  static constexpr bool ok = true;
-  static constexpr int R1 = 8, R2 = 6;
-};
-template <>
-struct TwoPass<64> {
-  static constexpr bool ok = true;
-  static constexpr int R1 = 16, R2 = 4;
-};
-template <>
-struct TwoPass<96> {
-  static constexpr bool ok = true;
-  static constexpr int R1 = 16, R2 = 6;
-};
-
+// results agree with it to rounding, not bitwise.  (TwoPass plans: dispatch.cuh.)
 template <int N>
 #ifndef PWB_PENCIL_H_MINB
 #define PWB_PENCIL_H_MINB 3   // 80-register cap; 3 CTAs/SM (smem 75 KB each)
@@ -556,6 +542,27 @@ int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, doub
   return PWB_OK;
 }
 
+int launch_pencil_to_cube_xmajor(pwb_grid* g, int nband, const double2* W, double scale,
+                                 double2* out) {
+  PWB_TRY(check_band_count(nband));
+  if (nband == 0) return PWB_OK;
+  PencilArgs a = empty_args();
+  a.win = W;
+  a.xin = g->dev.xa;
+  a.nxin = g->nxa;
+  a.in_stride = (size_t)g->nxa * g->nyz;
+  a.mode = 2;
+  a.cout = out;
+  a.out_stride = (size_t)g->ng;
+  a.oscale = scale;
+  dim3 grid(tiles(g), nband);
+  pencil_variant(g, [&](auto fx) {
+    (void)launch_k(k_pencil<0, 3, decltype(fx)>, grid, NT, pencil_smem(g), g->stream, g->dev, a);
+  });
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
 int launch_pencil_to_cube(pwb_grid* g, int nband, const double2* W, double scale, double2* out) {
   PWB_TRY(check_band_count(nband));
   if (nband == 0) return PWB_OK;
@@ -694,6 +701,8 @@ int configure_kernels(const pwb_grid* g) {
     }
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_pencil<0, 1, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_pencil<0, 3, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_pencil<0, 2, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
     if (e == cudaSuccess)

@@ -84,6 +84,9 @@ int launch_plane_fwd(pwb_grid* g, int nband, const int* band_k, const double2* W
                      const double2* psi_in, const double* shift, double2* out,
                      const int* rows = nullptr, const int* nact = nullptr);
 int launch_pencil_to_cube(pwb_grid* g, int nband, const double2* W, double scale, double2* out);
+// same, written x-major [band][x][yz] (the accumulation's psi(r) cache layout)
+int launch_pencil_to_cube_xmajor(pwb_grid* g, int nband, const double2* W, double scale,
+                                 double2* out);
 int launch_pencil_from_cube(pwb_grid* g, int nband, const double2* in, double2* W);
 // full-cube (all planes) helpers
 // mode: 0 no x-FFT, 1 forward, 2 inverse

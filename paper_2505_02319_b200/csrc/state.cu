@@ -81,7 +81,8 @@ static int ensure_psir(pwb_state* st, int b0, int b1) {
   const double2* phi = as<double2>(st->phi) + (size_t)b0 * g->nbp;
   const int* bk = as<int>(st->d_band_k) + b0;
   PWB_TRY(launch_plane_inv(g, n, bk, phi, 1.0, W));
-  PWB_TRY(launch_pencil_to_cube(g, n, W, 1.0 / std::sqrt(g->volume), as<double2>(st->psir)));
+  PWB_TRY(launch_pencil_to_cube_xmajor(g, n, W, 1.0 / std::sqrt(g->volume),
+                                       as<double2>(st->psir)));
   st->psir_b0 = b0;
   st->psir_b1 = b1;
   return PWB_OK;
@@ -325,7 +326,7 @@ int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, d
   cudaEvent_t ea = prof().begin(s);
   PWB_TRY(launch_plane_inv2(g, n, bk, as<double2>(st->dphi), as<double2>(cg.xr), W));
   const int ntile = (g->nyz + g->dev.tile - 1) / g->dev.tile;
-  int nchunk = std::max(1, std::min(n, (2 * kSM + ntile - 1) / ntile));
+  int nchunk = std::max(1, std::min(n, (3 * kSM + ntile - 1) / ntile));   // 3 CTAs per SM
   PWB_TRY(st->drho_part.ensure((size_t)nchunk * g->ng * sizeof(double)));
   PWB_TRY(launch_drho_partial(g, n, W, as<double2>(st->psir), c2, c1, nchunk,
                               as<double>(st->drho_part)));
