@@ -201,12 +201,6 @@ __global__ void __launch_bounds__(NTC) k_cg_beta(GridDev g, CgScalars sc, int n,
   if (threadIdx.x == 0) sc.rz[row] = rzn;
 }
 
-__global__ void k_zero2(int* c) {
-  pdl_wait();
-  c[0] = 0;
-  c[1] = 0;
-}
-
 // One CTA: active flags -> ascending active-row list, the stacked (x; r) list,
 // and the k-grouped projector tiles (<= kProjTileRows rows of one k block).
 // Rows are in k-block order, so each k's active rows are contiguous.
@@ -257,6 +251,8 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
     ctl.hdr[0] = na;
     ctl.hdr[1] = t;
     ctl.hdr[2] = 2 * t;
+    ctl.hdr[3] = 0;   // rows still iterating after this iteration (k_cg_resid counts)
+    ctl.hdr[4] = 0;   // max_iter failure flag
     carry = t;
   }
   __syncthreads();
@@ -428,9 +424,8 @@ static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s) {
                                cg.ctl.hdr + 2)))
       break;
     ec = prof().begin(s);
-    (void)launch_k(k_zero2, 1, 1, 0, s, cg.ctl.hdr + 3);
     (void)launch_k(k_cg_resid, n, NTC, 0, s, g->dev, cg.s, n, xr, z, rows, nact, cg.ctl.hdr + 3);
-    count_launch(2);
+    count_launch();
     prof().end(PROF_CG, ec, s, cg.prof_rows);
     cudaMemcpyAsync(cg.h_hdr, cg.ctl.hdr, 8 * sizeof(int), cudaMemcpyDeviceToHost, s);
     if ((status = project_rows(st, cg.pa, z, cg.s.active, n, rows, part, cmat, s, cg.ctl.hdr + 1)))

@@ -36,15 +36,13 @@ constexpr int KC = kProjChunk;      // sphere coefficients per pipeline chunk
 constexpr int MF = 5;               // m fragments per block
 constexpr int CM = 8 * MF;          // orbitals per block
 constexpr int NW = 8;               // warps per CTA
-constexpr int SC = 3;               // pipeline stages
+constexpr int SC = 4;               // apply pipeline stages (Phi blocks in flight)
+constexpr int SCC = 3;              // coef pipeline stages (X rows + Phi block)
 constexpr int RSC = kProjRowStride; // smem / chunk-major row stride (double2): 64 B mod 128 B
-constexpr int RSX = KC + 4;         // apply X row stride
-constexpr int RSM = CM + 4;         // apply C row stride (44 = 4 mod 8)
-constexpr int kCoefStage = (TR + CM) * RSC;              // double2 per coef stage
-constexpr int kApplyStage = CM * RSC + TR * RSX + TR * RSM;
-constexpr size_t kCoefSmem = (size_t)SC * kCoefStage * 16 + (size_t)(NW / 2) * CM * TR * 16 + 64;
-constexpr size_t kApplySmem = (size_t)SC * kApplyStage * 16 + 64;
-static_assert(kCoefSmem <= 232448 && kApplySmem <= 232448, "stage ring exceeds 227 KB");
+constexpr int kCoefStage = (TR + CM) * RSC;   // double2 per coef stage: X rows, Phi block
+constexpr int kApplyStage = CM * RSC;         // apply stage: one chunk-major Phi block
+constexpr size_t kCoefSmem = (size_t)SCC * kCoefStage * 16 + (size_t)(NW / 2) * CM * TR * 16 + 64;
+static_assert(kCoefSmem <= 232448, "stage ring exceeds 227 KB");
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -185,33 +183,44 @@ __device__ __forceinline__ const double2* phic_at(const ProjArgs& a, int k, int 
 }
 
 // Producer warp (warp NW) of the coef kernel: walks the same (item, chunk)
-// sequence as the consumers and keeps SC stages in flight; lane l copies X
-// row l, lane 31 the chunk's Phi block (one contiguous bulk copy of the
-// chunk-major layout).  Sources are resolved once per item.
+// sequence as the consumers and keeps SCC stages in flight.  The chunk's Phi
+// block is ONE contiguous TMA bulk copy (chunk-major layout); the up to 16
+// gathered X rows (1 KB each) go by cp.async from all 32 lanes, completing on
+// the same mbarrier (cp.async.mbarrier.arrive.noinc: 1 + 32 arrivals).  Sixteen
+// small bulk copies cost ~0.4 us more per stage than one (tools/tma_bw.cu).
+// Row sources are resolved once per item.
 __device__ void coef_producer(const ProjArgs& a, const CoefGeom& g, const double2* X,
                               double2* stages, uint64_t* full, uint64_t* empty, int lane) {
   CoefCursor c;
   c.first(a, g);
-  int cur = -1, nocc = 0;
-  const double2* xs = nullptr;
-  uint32_t bytes = 0;
+  int cur = -1, nocc = 0, nrows = 0;
+  const double2* xsrc = nullptr;   // row `lane` of the tile (lane < nrows)
   for (unsigned n = 0; c.valid; ++n) {
-    const int s = n % SC;
-    if (n >= SC) mbar_wait(&empty[s], ((n / SC) + 1) & 1);
+    const int s = n % SCC;
+    if (n >= SCC) mbar_wait(&empty[s], ((n / SCC) + 1) & 1);
     if (c.item != cur) {
       cur = c.item;
       nocc = a.nocc[c.it.t.k];
-      xs = lane < c.it.t.nrows ? X + (size_t)xrow(a, c.it.t, lane) * a.nbp : nullptr;
-      bytes = (uint32_t)c.it.t.nrows * KC * 16 + (uint32_t)c.it.nm * RSC * 16;
+      nrows = c.it.t.nrows;
+      xsrc = lane < nrows ? X + (size_t)xrow(a, c.it.t, lane) * a.nbp : nullptr;
+    }
+    double2* buf = stages + s * kCoefStage;
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)c.it.nm * RSC * 16;
+      mbar_expect_tx(&full[s], bytes);
+      bulk_g2s(buf + TR * RSC, phic_at(a, c.it.t.k, nocc, c.chunk, c.it.m0), bytes, &full[s]);
     }
     const size_t g0 = (size_t)c.chunk * KC;
-    double2* buf = stages + s * kCoefStage;
-    if (lane == 0) mbar_expect_tx(&full[s], bytes);
-    __syncwarp();
-    if (xs) bulk_g2s(buf + lane * RSC, xs + g0, KC * 16, &full[s]);
-    if (lane == 31)
-      bulk_g2s(buf + TR * RSC, phic_at(a, c.it.t.k, nocc, c.chunk, c.it.m0),
-               (uint32_t)c.it.nm * RSC * 16, &full[s]);
+    for (int p = lane; p < nrows * KC; p += 32) {   // 16-byte pieces, row r = p / KC
+      const int r = p / KC, o = p - r * KC;
+      const double2* src = reinterpret_cast<const double2*>(
+          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(xsrc), r));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(buf + r * RSC + o)),
+                   "l"(src + g0 + o)
+                   : "memory");
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(su32(&full[s]))
+                 : "memory");
     c.next(a, g);
   }
 }
@@ -223,17 +232,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
   double2* stages = sm;
-  double2* red = sm + SC * kCoefStage;   // [NW/2][CM][TR]
+  double2* red = sm + SCC * kCoefStage;   // [NW/2][CM][TR]
   uint64_t* full = reinterpret_cast<uint64_t*>(red + (NW / 2) * CM * TR);
-  uint64_t* empty = full + SC;
+  uint64_t* empty = full + SCC;
   __shared__ bool last;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r4 = lane >> 2, c4 = lane & 3;
   const CoefGeom g = coef_geom(a, nt_host, mtiles, smax);
   const size_t stride = (size_t)tile_cap * mtiles * (CM * TR);   // partials per split
   if (threadIdx.x == 0) {
-    for (int s = 0; s < SC; ++s) {
-      mbar_init(&full[s], 1);
+    for (int s = 0; s < SCC; ++s) {
+      mbar_init(&full[s], 1 + 32);   // TMA expect_tx arrival + 32 cp.async lanes
       mbar_init(&empty[s], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -261,8 +270,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
           t3[ma][nb][0] = t3[ma][nb][1] = 0.0;
         }
     }
-    const int s = seq % SC;
-    mbar_wait(&full[s], (seq / SC) & 1);
+    const int s = seq % SCC;
+    mbar_wait(&full[s], (seq / SCC) & 1);
     const double2* xs = stages + s * kCoefStage;
     const double2* ps = xs + TR * RSC;
     const int nfm = (it.nm + 7) >> 3, nfn = (it.t.nrows + 7) >> 3;
@@ -348,8 +357,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         if (last) {
           // Sum the splits of the valid entries in fixed order.  The splits are cut
           // into G contiguous groups summed by different threads (all loads of a
-          // group batch in flight together), then the groups are added in order:
-          // a handful of L2 round trips instead of one per 8 splits per entry.
+          // group batch in flight together), then the groups are added in order.
           __threadfence();
           const double2* p0 = part + tile_id * (CM * TR);
           const int nr = done.t.nrows;
@@ -389,69 +397,57 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
-// apply: work item = (tile, KC chunk of g); one stage per m block of the item
-// (C block + Phi block, plus the X chunk with the last m block).  Consumer
-// warp w owns the 8 g of fragment w for both row fragments.
+// apply: work item = (tile, KC chunk of g); each CTA takes a CONTIGUOUS range
+// of items (mostly one tile, so C is loaded once per tile run); one stage per
+// m block of the item = the chunk's Phi block (one bulk copy).  C rows of the
+// current tile live in smem (loaded by the consumers), X values of the
+// epilogue are loaded from global one item ahead.  Consumer warp w owns the
+// 8 g of fragment w for both row fragments.
 struct ApplyCursor {
-  int item, mblk, nitems, nchunk, nmb;
+  int item, item_end, mblk, nchunk, nmb, tile;
   ProjTile t;
   int nocc;
   bool valid;
   __device__ void load(const ProjArgs& a) {
-    const int tile = item / nchunk;
+    tile = item / nchunk;
     t = a.tiles[tile];
     nocc = a.nocc[t.k];
     nmb = (nocc + CM - 1) / CM;
   }
   __device__ void first(const ProjArgs& a, int ntiles) {
     nchunk = a.nbp / KC;
-    nitems = ntiles * nchunk;
-    item = blockIdx.x;
+    const int nitems = ntiles * nchunk;
+    const int per = (nitems + gridDim.x - 1) / gridDim.x;
+    item = blockIdx.x * per;
+    item_end = min(nitems, item + per);
     mblk = 0;
-    valid = item < nitems;
+    valid = item < item_end;
     if (valid) load(a);
   }
   __device__ void next(const ProjArgs& a) {
     if (++mblk < nmb) return;
     mblk = 0;
-    item += gridDim.x;
-    valid = item < nitems;
+    ++item;
+    valid = item < item_end;
     if (valid) load(a);
   }
 };
 
-// Producer warp of the apply kernel: lane 31 copies the chunk's Phi block (one
-// contiguous bulk copy), lane l < 16 X row l of the chunk, 16 <= l < 32 C row l - 16.
-__device__ void apply_producer(const ProjArgs& a, const double2* C, const double2* Xin,
-                               bool want_x, int ntiles, double2* stages, uint64_t* full,
-                               uint64_t* empty, int lane) {
+__device__ void apply_producer(const ProjArgs& a, int ntiles, double2* stages, uint64_t* full,
+                               uint64_t* empty, int nst, int lane) {
   ApplyCursor c;
   c.first(a, ntiles);
   for (unsigned n = 0; c.valid; ++n) {
-    const int s = n % SC;
-    if (n >= SC) mbar_wait(&empty[s], ((n / SC) + 1) & 1);
-    const int nr = c.t.nrows;
-    const int m0 = c.mblk * CM, nm = min(CM, c.nocc - m0);
-    const bool with_x = want_x && c.mblk == c.nmb - 1;
-    const int chunk = c.item % c.nchunk;
-    const size_t g0 = (size_t)chunk * KC;
-    const uint32_t bytes = (uint32_t)nm * RSC * 16 + (with_x ? (uint32_t)nr * KC * 16 : 0u) +
-                           (uint32_t)nr * nm * 16;
-    double2* ps = stages + s * kApplyStage;
-    double2* xs = ps + CM * RSC;
-    double2* cs = xs + TR * RSX;
-    if (lane == 0) mbar_expect_tx(&full[s], bytes);
-    __syncwarp();
-    if (lane == 31)
-      bulk_g2s(ps, phic_at(a, c.t.k, c.nocc, chunk, m0), (uint32_t)nm * RSC * 16, &full[s]);
-    if (lane < TR) {
-      if (with_x && lane < nr)
-        bulk_g2s(xs + lane * RSX, Xin + (size_t)xrow(a, c.t, lane) * a.nbp + g0, KC * 16,
-                 &full[s]);
-    } else if (lane - TR < nr) {
-      const int r = lane - TR;
-      bulk_g2s(cs + r * RSM, C + (size_t)(c.t.row0 + r) * a.ldc + m0, nm * 16, &full[s]);
+    const int s = n % nst;
+    if (n >= (unsigned)nst) mbar_wait(&empty[s], ((n / nst) + 1) & 1);
+    if (lane == 0) {
+      const int m0 = c.mblk * CM, nm = min(CM, c.nocc - m0);
+      const uint32_t bytes = (uint32_t)nm * RSC * 16;
+      mbar_expect_tx(&full[s], bytes);
+      bulk_g2s(stages + s * kApplyStage, phic_at(a, c.t.k, c.nocc, c.item % c.nchunk, m0), bytes,
+               &full[s]);
     }
+    __syncwarp();
     c.next(a);
   }
 }
@@ -459,17 +455,18 @@ __device__ void apply_producer(const ProjArgs& a, const double2* C, const double
 __global__ void __launch_bounds__((NW + 1) * 32, 1)
     k_proj_apply(ProjArgs a, const double2* __restrict__ C, const double2* __restrict__ Xin,
                  double2* __restrict__ Y, double ca, double cb, const int* __restrict__ active,
-                 int band_mod, int nt_host) {
+                 int band_mod, int nt_host, int csld, int nst) {
   pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + SC * kApplyStage);
+  double2* cs = sm + nst * kApplyStage;   // C rows of the current tile [TR][csld]
+  uint64_t* full = reinterpret_cast<uint64_t*>(cs + TR * csld);
   uint64_t* empty = full + SC;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r4 = lane >> 2, c4 = lane & 3;
   const int ntiles = a.ntiles ? *a.ntiles : nt_host;
   const bool want_x = ca != 0.0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < SC; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
     }
@@ -477,16 +474,35 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   }
   __syncthreads();
   if (w == NW) {
-    apply_producer(a, C, Xin, want_x, ntiles, sm, full, empty, lane);
+    apply_producer(a, ntiles, sm, full, empty, nst, lane);
     return;
   }
   ApplyCursor cons;
   cons.first(a, ntiles);
+  int cur_tile = -1;
+  int orow[2] = {-1, -1};   // output rows of this lane's fragment rows (-1: skip)
   // 3-multiplication complex product: t1 = sum cr pr, t2 = sum ci pi,
   // t3 = sum (cr + ci)(pr + pi);  Re = t1 - t2, Im = t3 - t1 - t2
   double t1[2][2], t2[2][2], t3[2][2];
+  double2 xv[2][2];   // epilogue X values [jb][h] of the current item
   unsigned seq = 0;
   while (cons.valid) {
+    if (cons.tile != cur_tile) {   // new tile: C rows -> smem, output rows
+      consumer_sync();             // every warp is done with the previous tile's C
+      cur_tile = cons.tile;
+      const int nr = cons.t.nrows, no = cons.nocc;
+      for (int i = threadIdx.x; i < nr * no; i += NW * 32) {
+        const int r = i / no, m = i - r * no;
+        cs[r * csld + m] = __ldg(&C[(size_t)(cons.t.row0 + r) * a.ldc + m]);
+      }
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb) {
+        const int r = 8 * jb + r4;
+        orow[jb] = r < nr ? xrow(a, cons.t, r) : -1;
+        if (orow[jb] >= 0 && active && !active[orow[jb] % band_mod]) orow[jb] = -1;
+      }
+      consumer_sync();
+    }
     if (cons.mblk == 0) {
 #pragma unroll
       for (int jb = 0; jb < 2; ++jb) {
@@ -494,13 +510,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         t2[jb][0] = t2[jb][1] = 0.0;
         t3[jb][0] = t3[jb][1] = 0.0;
       }
+      const size_t g0 = (size_t)(cons.item % cons.nchunk) * KC;
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb)   // in flight during the item's DMMAs
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          xv[jb][h] = (want_x && orow[jb] >= 0)
+                          ? __ldg(&Xin[(size_t)orow[jb] * a.nbp + g0 + 8 * w + 2 * c4 + h])
+                          : make_double2(0.0, 0.0);
     }
-    const int s = seq % SC;
-    mbar_wait(&full[s], (seq / SC) & 1);
+    const int s = seq % nst;
+    mbar_wait(&full[s], (seq / nst) & 1);
     const double2* ps = sm + s * kApplyStage;
-    const double2* xs = ps + CM * RSC;
-    const double2* cs = xs + TR * RSX;
-    const int nm = min(CM, cons.nocc - cons.mblk * CM);
+    const int m0 = cons.mblk * CM, nm = min(CM, cons.nocc - m0);
     const int nfn = (cons.t.nrows + 7) >> 3;
 #pragma unroll 2
     for (int ms = 0; ms < nm; ms += 4) {
@@ -509,10 +531,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
       double2 av[2];
 #pragma unroll
       for (int jb = 0; jb < 2; ++jb)   // A[j = r4][k = c4] = C[row j][m]
-        av[jb] = (mok && jb < nfn) ? cs[(8 * jb + r4) * RSM + m] : make_double2(0.0, 0.0);
+        av[jb] = (mok && jb < nfn) ? cs[(8 * jb + r4) * csld + m0 + m] : make_double2(0.0, 0.0);
       const double2 bv = mok ? ps[m * RSC + 8 * w + r4] : make_double2(0.0, 0.0);   // Phi[m][g]
       const double bs = bv.x + bv.y;
-      // C * Phi : re = cr pr - ci pi ; im = cr pi + ci pr  (3 real products)
 #pragma unroll
       for (int jb = 0; jb < 2; ++jb) {
         if (jb >= nfn) break;
@@ -521,31 +542,27 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         dmma(t3[jb][0], t3[jb][1], av[jb].x + av[jb].y, bs);
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
     if (cons.mblk == cons.nmb - 1) {   // epilogue: D fragment row j = r4, g = 2 c4 + {0,1}
       const size_t g0 = (size_t)(cons.item % cons.nchunk) * KC;
 #pragma unroll
       for (int jb = 0; jb < 2; ++jb) {
-        const int r = 8 * jb + r4;
-        if (r >= cons.t.nrows) continue;
-        const int row = xrow(a, cons.t, r);
-        if (active && !active[row % band_mod]) continue;
+        const int row = orow[jb];
+        if (row < 0) continue;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int gl = 8 * w + 2 * c4 + h;
-          const double2 x = want_x ? xs[r * RSX + gl] : make_double2(0.0, 0.0);
           const double dr = t1[jb][h] - t2[jb][h];
           const double di = t3[jb][h] - t1[jb][h] - t2[jb][h];
-          Y[(size_t)row * a.nbp + g0 + gl] = make_double2(ca * x.x + cb * dr, ca * x.y + cb * di);
+          Y[(size_t)row * a.nbp + g0 + 8 * w + 2 * c4 + h] =
+              make_double2(ca * xv[jb][h].x + cb * dr, ca * xv[jb][h].y + cb * di);
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
     ++seq;
     cons.next(a);
   }
 }
-
 
 // ---------------------------------------------------------------------------
 static int proj_configure() {
@@ -554,7 +571,7 @@ static int proj_configure() {
   PWB_CUDA(cudaFuncSetAttribute(k_proj_coef, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kCoefSmem));
   PWB_CUDA(cudaFuncSetAttribute(k_proj_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kApplySmem));
+                                232448));
   done = true;
   return PWB_OK;
 }
@@ -647,9 +664,13 @@ int proj_apply(const ProjPlan& pl, ProjArgs a, const double2* C, const double2* 
   a.nrows_total = pl.nrows;
   const long items = (long)cap * (a.nbp / KC);
   const int grid = (int)std::min<long>(items, kSM);
-  (void)launch_k(k_proj_apply, grid, (NW + 1) * 32, kApplySmem, st, a, C, Xin, Y, ca, cb, active,
-                                                  band_mod > 0 ? band_mod : 1,
-                                                  (int)pl.tiles.size());
+  const int csld = ((a.ldc + 3) / 8) * 8 + 4;   // C rows in smem: stride = 4 mod 8 (conflict-free)
+  int nst = SC;   // fewer Phi stages in flight when many orbitals' C rows take the smem
+  while (nst > 2 && (size_t)nst * kApplyStage * 16 + (size_t)TR * csld * 16 + 64 > 232448) --nst;
+  const size_t smem = (size_t)nst * kApplyStage * 16 + (size_t)TR * csld * 16 + 64;
+  if (smem > 232448) return fail(PWB_ERR_UNSUPPORTED, "projector: too many orbitals per k");
+  (void)launch_k(k_proj_apply, grid, (NW + 1) * 32, smem, st, a, C, Xin, Y, ca, cb, active,
+                 band_mod > 0 ? band_mod : 1, (int)pl.tiles.size(), csld, nst);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
