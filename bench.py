@@ -202,9 +202,38 @@ def roofline_from_profile(prof, gs):
     }
 
 
-def oracle_sample(gs, dv0, params, budget_s):
+def projector_roofline(prof, gs, peak_fp64):
+    """FP64 roofline of the projector GEMM group over the profiled solve.
+
+    F_Q = 16 N_b N_occ flop per row per Q application (two complex
+    GEMMs, 8 flop per complex MAC); rows = the live rows of every projector call
+    (x and r count twice), N_occ the row-weighted mean over k blocks."""
+    from paper_2505_02319_b200.device import state_blocks
+    blocks, _ = state_blocks(gs)
+    nocc = np.array([b.n_occ for b in blocks], dtype=float)
+    nb = np.array([b.grids.n_b for b in blocks], dtype=float)
+    f_row = 16.0 * float(np.sum(nocc * nb * nocc) / np.sum(nocc))
+    ms, count, units = prof["projector"]
+    achieved = f_row * units / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    return {"kernel": "projector Q X (k_proj_coef + k_proj_apply), all CG calls of one solve",
+            "bound": "tensor", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s (FP64)",
+            "frac": achieved / peak_fp64, "traffic": None,
+            "peak_source": "measured live: cuBLAS DGEMM 8192^3 best of 5",
+            "algorithmic_flop_per_row": f_row, "rows": int(units), "launch_pairs": int(count),
+            "avg_rows_per_call": units / max(count, 1)}
+
+
+def oracle_sample(gs, dv0, params, budget_s, threads=1):
     """Bounded CPU sample of the workload: the oracle's RHS + Sternheimer solves of
-    the first (k, n) pairs at the solve's iteration-0 tolerances, band-applies/s."""
+    the first (k, n) pairs at the solve's iteration-0 tolerances, band-applies/s.
+
+    BLAS is pinned to one thread; `threads` > 1 runs the bands on a thread pool,
+    the reference's own band parallelism (response.py:144-148, scipy.fft and
+    OpenBLAS release the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from threadpoolctl import threadpool_limits
+
     from oracle import dyson as od
     from oracle import model as om
     from oracle import outer as oo
@@ -213,23 +242,36 @@ def oracle_sample(gs, dv0, params, budget_s):
     spec = oo.parse(params["strategy"], params["tau"], params["m"])
     nrm = float(np.linalg.norm(dv0))
     tols = od.tolerance_vector(og, spec, 0, kv_norm=nrm, rhs_norm=1.0)
-    blk = og.blocks[0] if hasattr(og, "blocks") else og
-    t0 = time.perf_counter()
-    start = om.ham_counter.value
-    b = blk.grids
-    done = 0
+    blocks = og.blocks if hasattr(og, "blocks") else [og]
+    pairs, off = [], 0
+    for blk in blocks:                      # (k, n) pairs in the solve's order
+        pairs += [(blk, n, off + n) for n in range(blk.n_occ)]
+        off += blk.n_occ
     dv = dv0 / nrm
-    for n in range(blk.n_occ):
+
+    def one(pair):
+        blk, n, i = pair
+        b = blk.grids
         pr = b.to_real(blk.phi[:, n])
         rhs = -orsp.project_out(blk.phi_occ, b.to_fourier(dv * pr))
-        orsp.sternheimer(blk, blk.v_local, n, rhs, tols[n])
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    nh = om.ham_counter.value - start
-    return nh / dt, f"{done} (k=0, n) Sternheimer solves with RHS FFTs at the iteration-0 " \
-                    f"tolerances ({nh} band-applies in {dt:.1f} s), oracle/ numpy port, 1 thread"
+        orsp.sternheimer(blk, blk.v_local, n, rhs, tols[i])
+
+    done = 0
+    with threadpool_limits(limits=1), ThreadPoolExecutor(max_workers=threads) as pool:
+        t0 = time.perf_counter()
+        start = om.ham_counter.value
+        while done < len(pairs):
+            batch = pairs[done:done + threads]
+            list(pool.map(one, batch))
+            done += len(batch)
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        nh = om.ham_counter.value - start
+    how = "1 thread" if threads == 1 else f"{threads}-thread band pool"
+    return nh / dt, f"first {done} of {len(pairs)} (k, n) Sternheimer solves of the RHS chi0 " \
+                    f"apply, with their RHS FFTs, at the iteration-0 tolerances ({nh} " \
+                    f"band-applies in {dt:.1f} s), oracle/ numpy port, {how}, BLAS 1 thread"
 
 
 def cpu_baseline(gs, dv0, params, budget_s):
@@ -242,16 +284,18 @@ def cpu_baseline(gs, dv0, params, budget_s):
         return {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
     og = to_oracle(gs)
     spec = oo.parse(params["strategy"], params["tau"], params["m"])
-    t0 = time.perf_counter()
-    n_ham, solves = 0, 0
-    while True:
-        start = om.ham_counter.value
-        res = od.solve(og, dv0, spec, xc=params["xc"])
-        n_ham += om.ham_counter.value - start
-        solves += 1
-        if time.perf_counter() - t0 > budget_s or solves >= 20:
-            break
-    dt = time.perf_counter() - t0
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        n_ham, solves = 0, 0
+        while True:
+            start = om.ham_counter.value
+            res = od.solve(og, dv0, spec, xc=params["xc"])
+            n_ham += om.ham_counter.value - start
+            solves += 1
+            if time.perf_counter() - t0 > budget_s or solves >= 20:
+                break
+        dt = time.perf_counter() - t0
     return {"value": n_ham / dt, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"{solves} full Dyson solve(s) of the same workload, oracle/ numpy port "
                       f"(scipy.fft + OpenBLAS, 1 thread); {dt / solves * 1e3:.1f} ms per solve",
@@ -279,6 +323,164 @@ def to_oracle(gs):
 
 
 # ----------------------------------------------------------------------------------------
+# BASELINE configs[3]: kernel microbench (one batched H apply + one projected-CG iteration)
+
+def fp64_peak(dev):
+    """Measured FP64 tensor throughput of this GPU: cuBLAS DGEMM 8192^3, best of 5 (TFLOP/s)."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, a)
+    best = float("inf")
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+class _MicroState:
+    """GroundState-shaped holder for configs[3]'s random orthonormal bands."""
+
+    def __init__(self, grids, phi, eps, v_local):
+        self.grids, self.phi_occ, self.eps_occ, self.v_local = grids, phi, eps, v_local
+        self.n_occ = phi.shape[1]
+        self.occ_occ = np.full(self.n_occ, 2.0)
+        self.rho = np.zeros_like(v_local)
+
+    def fprime_occ(self):
+        return np.zeros(self.n_occ)
+
+
+def run_microbench(args):
+    """configs[3]: 96^3 cube, 256 random orthonormal bands (Phi = the bands), V ~ U(-1,1)
+    smoothed; eps_n = Re <psi_n, H psi_n>; step = one batched projected-CG iteration of
+    the 256 Sternheimer rows rhs_n = -Q(V psi_n) through the C-ABI (pwb_sternheimer:
+    init projection + one iteration = 1 batched H apply + 5 Q, the reference op
+    sequence, sternheimer.py:59-91).  Separately timed: the batched H apply alone
+    (HBM roofline) and one Q on the 256 rows (FP64 roofline)."""
+    import ctypes
+
+    import torch
+
+    from paper_2505_02319_b200 import _lib, ops, synth
+    from paper_2505_02319_b200.device import device_state, ptr
+    from paper_2505_02319_b200.pwbasis import Lattice, build_grids
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    p, _, rng = synth.model_parameters(3)
+    g = build_grids(Lattice.from_vectors(*synth.cell_vectors(p["cell"])), p["e_cut"])
+    nb = 256
+    phi = synth.random_orthonormal(rng, g.n_b, nb)
+    v = synth.smoothed_uniform(g.g2_cube, g.cube_dims, rng)
+    eps = np.zeros(nb)
+    ms0 = _MicroState(g, phi, eps, v)
+    ds = device_state(ms0)
+    dg = ds.grid
+    vt = torch.from_numpy(v).to(dev)
+    psi = dg.pack(list(phi.T))
+    hpsi = ops.ham_apply_dev(dg, psi, vt)
+    eps[:] = torch.sum(psi.conj() * hpsi, dim=1).real.cpu().numpy()
+    ms = _MicroState(g, phi, eps, v)          # eps known now: the state the CG uses
+    ds = device_state(ms)
+    lib = _lib.load()
+    # rhs_n = -Q (V psi_n): V psi in the sphere basis, then the projector
+    rhs = -ops.to_fourier_many_dev(dg, ops.to_real_many_dev(dg, psi) * vt[None, :])
+    _lib.check(lib.pwb_project_out(ds.handle, 0, nb, ptr(rhs)), "project_out")
+    bands = np.arange(nb, dtype=np.int32)
+    tol = np.full(nb, 1e300)                     # every row stops after its one iteration
+    x = torch.zeros_like(rhs)
+    its = np.zeros(nb, dtype=np.int32)
+    res = np.zeros(nb)
+
+    def step():
+        _lib.check(lib.pwb_sternheimer(ds.handle, nb, ctypes.c_void_p(bands.ctypes.data),
+                                       ptr(rhs), ctypes.c_void_p(tol.ctypes.data), 0, ptr(x),
+                                       ctypes.c_void_p(its.ctypes.data),
+                                       ctypes.c_void_p(res.ctypes.data)), "sternheimer")
+
+    def timed(fn, reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        step()
+    assert np.all(its == 1)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.launch_count()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        step_ms.append(timed(step, 1))
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    ms_step = float(np.mean(step_ms))
+    # the two kernel groups alone (inputs larger than L2: 256 rows x 50 685 x 16 B = 207 MB)
+    out = dg.rows(nb)
+    h_ms = timed(lambda: lib.pwb_ham_apply(dg.handle, nb, None, ptr(psi), ptr(vt), None,
+                                           ptr(out)), 5)
+    y = rhs.clone()
+    q_ms = timed(lambda: lib.pwb_project_out(ds.handle, 0, nb, ptr(y)), 5)
+    # e2e: host rhs in, host solution out, through the host-buffer C-ABI path
+    pinned_in = rhs.cpu().pin_memory()
+    pinned_out = torch.empty_like(pinned_in, device="cpu").pin_memory()
+    rhs_dev = torch.empty_like(rhs)
+
+    def e2e_step():
+        rhs_dev.copy_(pinned_in, non_blocking=True)
+        _lib.check(lib.pwb_sternheimer(ds.handle, nb, ctypes.c_void_p(bands.ctypes.data),
+                                       ptr(rhs_dev), ctypes.c_void_p(tol.ctypes.data), 0,
+                                       ptr(x), ctypes.c_void_p(its.ctypes.data),
+                                       ctypes.c_void_p(res.ctypes.data)), "sternheimer")
+        pinned_out.copy_(x, non_blocking=True)
+    e2e_ms = timed(e2e_step, max(1, args.steps))
+    peak_hbm, how = peaks()
+    peak_fp64 = fp64_peak(dev)
+    b_h = 64.0 * g.n_g + 32.0 * g.n_b
+    f_q = 16.0 * g.n_b * nb * nb
+    line = {"metric": "H*psi band-applies/s (batched H apply + projected-CG iteration)",
+            "value": nb / (ms_step * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic",
+            "config": {"workload": "BASELINE configs[3]: one batched H apply + projected-CG "
+                                   "iteration (init Q + 1 iteration, 5 Q) on 256 bands",
+                       "cube": list(g.cube_dims), "n_b": int(g.n_b), "bands": nb,
+                       "n_occ": nb, "cell": "cubic 20 bohr", "e_cut": p["e_cut"],
+                       "l2": "flushed (256 MiB write) between timed steps; operands 207 MB"},
+            "step_ms": [round(t, 3) for t in step_ms], "gpu_launches": int(launches),
+            "clocks": clk,
+            "e2e": {"value": nb / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(rhs.numel() * 16),
+                    "d2h_bytes_per_step": int(x.numel() * 16), "ms_per_step": e2e_ms},
+            "roofline": {"kernel": "ham_apply (batched, 256 bands)", "bound": "hbm",
+                         "achieved": b_h * nb / (h_ms * 1e-3) / 1e9, "peak": peak_hbm,
+                         "unit": "GB/s", "frac": b_h * nb / (h_ms * 1e-3) / 1e9 / peak_hbm,
+                         "traffic": None, "peak_source": how, "avg_launch_ms": h_ms,
+                         "algorithmic_bytes_per_band_apply": b_h},
+            "roofline_projector": {"kernel": "projector Q X (coef + apply GEMMs, 256 x 256 "
+                                             "orbitals)", "bound": "tensor",
+                                   "achieved": f_q / (q_ms * 1e-3) / 1e12, "peak": peak_fp64,
+                                   "unit": "TFLOP/s (FP64)",
+                                   "frac": f_q / (q_ms * 1e-3) / 1e12 / peak_fp64,
+                                   "traffic": None,
+                                   "peak_source": "measured live: cuBLAS DGEMM 8192^3 best of 5",
+                                   "avg_launch_ms": q_ms,
+                                   "algorithmic_flop_per_launch": f_q}}
+    print(json.dumps(line))
+
 
 def run_reference(args):
     """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
@@ -287,11 +489,12 @@ def run_reference(args):
         return
     import multiprocessing
     gs, dv0, params = build_workload(args.config)
+    ncores = len(os.sched_getaffinity(0))
     if hasattr(gs, "blocks") or gs.grids.n_g > 100000:
         vals = []
         t_all = time.perf_counter()
         for _ in range(args.warmup + args.steps):
-            v, sample = oracle_sample(gs, dv0, params, 20.0)
+            v, sample = oracle_sample(gs, dv0, params, 20.0, threads=ncores)
             vals.append(v)
         value = float(np.mean(vals[args.warmup:]))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
@@ -300,7 +503,7 @@ def run_reference(args):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64/c128", "data": "synthetic",
                 "config": workload_desc(args.config, gs, params),
-                "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
                                  "sample": "per step: " + sample +
                                  f" (host has {multiprocessing.cpu_count()} cores)"},
                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -310,26 +513,31 @@ def run_reference(args):
     from oracle import dyson as od
     from oracle import model as om
     from oracle import outer as oo
+    from threadpoolctl import threadpool_limits
+
+    from oracle import response as orsp
     og = to_oracle(gs)
     spec = oo.parse(params["strategy"], params["tau"], params["m"])
-    for _ in range(args.warmup):
-        od.solve(og, dv0, spec, xc=params["xc"])
-    t0 = time.perf_counter()
-    n_ham = 0
-    for _ in range(args.steps):
-        start = om.ham_counter.value
-        od.solve(og, dv0, spec, xc=params["xc"])
-        n_ham += om.ham_counter.value - start
-    dt = time.perf_counter() - t0
+    orsp.BAND_THREADS = cores = ncores
+    with threadpool_limits(limits=1):
+        for _ in range(args.warmup):
+            od.solve(og, dv0, spec, xc=params["xc"])
+        t0 = time.perf_counter()
+        n_ham = 0
+        for _ in range(args.steps):
+            start = om.ham_counter.value
+            od.solve(og, dv0, spec, xc=params["xc"])
+            n_ham += om.ham_counter.value - start
+        dt = time.perf_counter() - t0
     value = n_ham / dt
-    cores = 1
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic",
             "config": workload_desc(args.config, gs, params),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full Dyson solves, oracle/ numpy port "
+                             "sample": f"{args.steps} full Dyson solves, oracle/ numpy port, "
+                                       f"{ncores}-thread band pool, BLAS 1 thread "
                                        f"(host has {multiprocessing.cpu_count()} cores)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -340,6 +548,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 3:
+        return run_microbench(args)
     world, rank, local = dist_env()
     import torch
     torch.cuda.set_device(local)
@@ -407,7 +617,7 @@ def main():
 
     # ---- e2e: public API with host buffers ------------------------------------------
     pinned = torch.from_numpy(dv0).pin_memory()
-    e2e_ms, e2e_ham = 0.0, 0
+    e2e_ms, e2e_ham, e2e_list = 0.0, 0, []
     e2e_steps = max(1, min(args.steps, 3))
     barrier()
     for _ in range(e2e_steps):
@@ -420,7 +630,8 @@ def main():
         sol = r.solution.cpu()
         e1.record()
         torch.cuda.synchronize()
-        e2e_ms += e0.elapsed_time(e1)
+        e2e_list.append(e0.elapsed_time(e1))
+        e2e_ms += e2e_list[-1]
         e2e_ham += r.n_ham
         del sol
     if world > 1:
@@ -429,7 +640,7 @@ def main():
         e2e_ms = float(t.item())
     e2e = {"value": e2e_ham / (e2e_ms * 1e-3), "unit": UNIT,
            "h2d_bytes_per_step": int(dv0.nbytes), "d2h_bytes_per_step": int(dv0.nbytes),
-           "ms_per_step": e2e_ms / e2e_steps}
+           "ms_per_step": e2e_ms / e2e_steps, "step_ms": [round(t, 3) for t in e2e_list]}
 
     if rank != 0:
         if world > 1:
@@ -444,6 +655,7 @@ def main():
             "step_ms": [round(t, 3) for t in step_ms],
             "gpu_launches": int(launches), "clocks": clk, "e2e": e2e,
             "roofline": roofline_from_profile(prof, gs),
+            "roofline_projector": projector_roofline(prof, gs, fp64_peak(dev)),
             "kernel_ms_by_live_rows": {
                 cat: {f">={1 << b}": [round(ms, 2), n] for b, ms, n in rows}
                 for cat, rows in hist.items() if cat in ("ham_apply", "projector", "cg_vector")}}

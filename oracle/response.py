@@ -15,6 +15,7 @@ a global delta eps_F; each k block is processed with the Gamma code on its
 k-shifted basis.
 """
 
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -25,6 +26,7 @@ PRECOND_FLOOR = 0.1            # sternheimer.py:19
 DEGENERACY_RTOL = 1e-8         # response.py:25
 IMAG_RTOL = 1e-10              # response.py:26
 LDA_FLOOR = 1e-10              # kernels.py:16
+BAND_THREADS = 1               # Sternheimer band pool width (response.py:144-148)
 
 
 def project_out(phi, x):
@@ -138,10 +140,15 @@ def _chi0_block(gs, dv, tols, de_f=None, weight=1.0):
     de = np.diag(m).real
     fp = gs.fprime_occ()
     dphi_p = gs.phi_occ @ (pair_weights(gs) * m)
-    results = []
-    for n in range(gs.n_occ):
+    def one(n):
         rhs = -project_out(gs.phi_occ, dvpsi[n])
-        results.append(sternheimer(gs, gs.v_local, n, rhs, tols[n]))
+        return sternheimer(gs, gs.v_local, n, rhs, tols[n])
+
+    if BAND_THREADS > 1:   # the reference's band pool (response.py:144-148); same results
+        with ThreadPoolExecutor(max_workers=BAND_THREADS) as pool:
+            results = list(pool.map(one, range(gs.n_occ)))
+    else:
+        results = [one(n) for n in range(gs.n_occ)]
     return dict(pr=pr, de=de, fp=fp, dphi_p=dphi_p, results=results, weight=weight)
 
 

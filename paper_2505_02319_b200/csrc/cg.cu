@@ -295,14 +295,14 @@ ProjArgs proj_args(pwb_state* st) {
 // Q X in place for the rows of a plan (masked by `active` when given)
 int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* active, int band_mod,
                  const int* rows, double2* part, double2* cmat, cudaStream_t s,
-                 const int* ntiles) {
+                 const int* ntiles, int mult) {
   ProjArgs a = proj_args(st);
   a.rows = rows;
   a.ntiles = ntiles;
   cudaEvent_t e = prof().begin(s);
   PWB_TRY(proj_coeffs(pl, a, X, part, cmat, s));
   PWB_TRY(proj_apply(pl, a, cmat, X, X, 1.0, -1.0, active, band_mod, s));
-  prof().end(PROF_Q, e, s, prof().rows_hint > 0 ? prof().rows_hint : pl.nrows);
+  prof().end(PROF_Q, e, s, prof().rows_hint > 0 ? (long long)mult * prof().rows_hint : pl.nrows);
   return PWB_OK;
 }
 
@@ -421,7 +421,7 @@ static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s) {
     count_launch();
     prof().end(PROF_CG, ec, s, cg.prof_rows);
     if ((status = project_rows(st, cg.pb, xr, cg.s.active, n, cg.ctl.rows2, part, cmat, s,
-                               cg.ctl.hdr + 2)))
+                               cg.ctl.hdr + 2, 2)))   // x and r rows together
       break;
     ec = prof().begin(s);
     (void)launch_k(k_cg_resid, n, NTC, 0, s, g->dev, cg.s, n, xr, z, rows, nact, cg.ctl.hdr + 3);

@@ -59,7 +59,7 @@ constexpr int kMaxK = 128;  // k blocks handled by the device-side compaction
 ProjArgs proj_args(pwb_state* st);
 int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* active, int band_mod,
                  const int* rows, double2* part, double2* cmat, cudaStream_t s,
-                 const int* ntiles = nullptr);
+                 const int* ntiles = nullptr, int mult = 1);
 int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands);
 int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max_iter,
              int* iters_host, double* res_host);
