@@ -99,11 +99,14 @@ __global__ void __launch_bounds__(NTA, 3) k_drho_h(GridDev g, int nband, int per
   const int tid = threadIdx.x;
   const int ja = tid / LP1, la = tid - ja * LP1;   // pass A: butterfly ja of lines la, la + LP1..
   const int jb = tid / LP2, lb = tid - jb * LP2;   // pass B: butterfly jb of lines lb + m LP2
-  double2 w[R2];
+  constexpr bool kHoldW = R2 <= 8;   // radix 12: twiddles from L1 per use (registers)
+  double2 w[kHoldW ? R2 : 1];
+  if constexpr (kHoldW) {
 #pragma unroll
-  for (int r = 1; r < R2; ++r) {
-    const double2 t = __ldg(&g.px.tw[r * jb]);
-    w[r] = make_double2(t.x, -t.y);   // inverse
+    for (int r = 1; r < R2; ++r) {
+      const double2 t = __ldg(&g.px.tw[r * jb]);
+      w[r] = make_double2(t.x, -t.y);   // inverse
+    }
   }
   double acc[MB][R2];
 #pragma unroll
@@ -141,7 +144,14 @@ __global__ void __launch_bounds__(NTA, 3) k_drho_h(GridDev g, int nband, int per
           p[r] = __ldg(&ps[(size_t)(jb + r * R1) * nyz + l]);
         }
 #pragma unroll
-        for (int r = 1; r < R2; ++r) v[r] = cmul(v[r], w[r]);
+        for (int r = 1; r < R2; ++r) {
+          if constexpr (kHoldW) {
+            v[r] = cmul(v[r], w[r]);
+          } else {
+            const double2 t = __ldg(&g.px.tw[r * jb]);
+            v[r] = cmul(v[r], make_double2(t.x, -t.y));
+          }
+        }
         Dft<R2>::run(v, 1.0);   // outputs x = jb + r R1 (natural order)
 #pragma unroll
         for (int r = 0; r < R2; ++r)

@@ -24,9 +24,13 @@ struct TwoPass<64> {
   static constexpr int R1 = 16, R2 = 4;
 };
 template <>
-struct TwoPass<96> {
-  static constexpr bool ok = true;
+struct TwoPass<96> {   // 8 x 12: radix-16 lines held in registers spilled at 80 registers
+  static constexpr bool ok = true;  // (ncu at 96^3: STL/LDL a quarter of the pencil's stalls)
+#ifdef PWB_TWOPASS96_16x6
   static constexpr int R1 = 16, R2 = 6;
+#else
+  static constexpr int R1 = 8, R2 = 12;
+#endif
 };
 
 // ----------------------------------------------------------------------------

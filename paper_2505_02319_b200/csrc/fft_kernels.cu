@@ -21,9 +21,21 @@ constexpr int NT = 256;
 #endif
 
 // ----------------------------------------------------------------------------
-// plane pass, inverse: sphere rows -> W[b][p]
+// Threads per plane CTA: planes too large for 3 resident CTAs per SM (96 x 96,
+// 32 x 320: 150-170 KB of smem, one CTA per SM) get 512 threads so that an SM
+// still has 16 warps to hide the global and barrier latency (ncu at 96^3:
+// 12% warps active, 1.7 TB/s with 256 threads).
+#ifndef PWB_PLANE_BIG_NT
+#define PWB_PLANE_BIG_NT 512
+#endif
 template <class FY, class FZ>
-__global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_inv(GridDev g, const double2* __restrict__ psi,
+constexpr int plane_nt() {
+  return (FY::N * FZ::N > 4800) ? PWB_PLANE_BIG_NT : NT;
+}
+
+// plane pass, inverse: sphere rows -> W[b][p]
+template <class FY, class FZ, int PT = plane_nt<FY, FZ>()>
+__global__ void __launch_bounds__(PT, PT == NT ? PWB_FFT_MINB : 1) k_plane_inv(GridDev g, const double2* __restrict__ psi,
                                                   const double2* __restrict__ psi2,
                                                   const int* __restrict__ band_k, double scale,
                                                   double2* __restrict__ W,
@@ -41,7 +53,7 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_inv(GridDev g, const
   const int nz = FZ::N ? FZ::N : g.nz;
   const int nyz = ny * nz;
   const int nyp = FY::N ? (FY::N % 2 == 0 ? FY::N + 1 : FY::N) : g.nyp;   // odd smem stride
-  for (int i = threadIdx.x; i < nz * nyp; i += NT) sm[i] = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < nz * nyp; i += PT) sm[i] = make_double2(0.0, 0.0);
   __syncthreads();
   const int s0 = g.xr[k * (g.nxa + 1) + p];
   const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
@@ -49,15 +61,15 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_inv(GridDev g, const
   const int* pp = g.ppp + (size_t)k * g.nbp;
   if (psi2) {
     const double2* src2 = psi2 + (size_t)row * g.nbp;
-    for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(cadd(src[s], src2[s]), scale);
+    for (int s = s0 + threadIdx.x; s < s1; s += PT) sm[pp[s]] = cscale(cadd(src[s], src2[s]), scale);
   } else {
-    for (int s = s0 + threadIdx.x; s < s1; s += NT) sm[pp[s]] = cscale(src[s], scale);
+    for (int s = s0 + threadIdx.x; s < s1; s += PT) sm[pp[s]] = cscale(src[s], scale);
   }
   __syncthreads();
-  FZ::template run<NT>(g, sm, g.nya, nyp, 0, g.ya, true);    // z lines of active y
-  FY::template run<NT>(g, sm, nz, 1, nyp, nullptr, true, 0);  // y lines, threads across lines
+  FZ::template run<PT>(g, sm, g.nya, nyp, 0, g.ya, true);    // z lines of active y
+  FY::template run<PT>(g, sm, nz, 1, nyp, nullptr, true, 0);  // y lines, threads across lines
   double2* dst = W + ((size_t)b * g.nxa + p) * nyz;
-  for (int i = threadIdx.x; i < nyz; i += NT) {
+  for (int i = threadIdx.x; i < nyz; i += PT) {
     const int z = i / ny;
     dst[i] = sm[i + z * (nyp - ny)];
   }
@@ -65,8 +77,8 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_inv(GridDev g, const
 
 // plane pass, forward: W[b][p] -> sphere rows with epilogue
 //   out[s] = a * F(W)[pp[s]] + (kin[s] - shift[b]) * psi_in[s]
-template <class FY, class FZ>
-__global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_fwd(GridDev g, const double2* __restrict__ W,
+template <class FY, class FZ, int PT = plane_nt<FY, FZ>()>
+__global__ void __launch_bounds__(PT, PT == NT ? PWB_FFT_MINB : 1) k_plane_fwd(GridDev g, const double2* __restrict__ W,
                                                   const int* __restrict__ band_k, double a,
                                                   const double2* __restrict__ psi_in,
                                                   const double* __restrict__ shift,
@@ -85,12 +97,12 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_fwd(GridDev g, const
   const int nyz = ny * nz;
   const int nyp = FY::N ? (FY::N % 2 == 0 ? FY::N + 1 : FY::N) : g.nyp;
   const double2* srcw = W + ((size_t)slot * g.nxa + p) * nyz;
-  staged_copy<8, NT>(
+  staged_copy<8, PT>(
       nyz, [&](int i) { return __ldg(&srcw[i]); },
       [&](int i, double2 v) { sm[i + (i / ny) * (nyp - ny)] = v; });
   __syncthreads();
-  FY::template run<NT>(g, sm, nz, 1, nyp, nullptr, false, 0);  // y lines, every z
-  FZ::template run<NT>(g, sm, g.nya, nyp, 0, g.ya, false);       // z lines of active y
+  FY::template run<PT>(g, sm, nz, 1, nyp, nullptr, false, 0);  // y lines, every z
+  FZ::template run<PT>(g, sm, g.nya, nyp, 0, g.ya, false);       // z lines of active y
   const int s0 = g.xr[k * (g.nxa + 1) + p];
   const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
   const int* pp = g.ppp + (size_t)k * g.nbp;
@@ -99,14 +111,14 @@ __global__ void __launch_bounds__(NT, PWB_FFT_MINB) k_plane_fwd(GridDev g, const
   const double sh = shift ? shift[b] : 0.0;
   if (psi_in) {
     const double2* pin = psi_in + (size_t)b * g.nbp;
-    for (int s = s0 + threadIdx.x; s < s1; s += NT) {
+    for (int s = s0 + threadIdx.x; s < s1; s += PT) {
       const double2 v = sm[pp[s]];
       const double2 q = pin[s];
       const double d = kin[s] - sh;
       dst[s] = make_double2(a * v.x + d * q.x, a * v.y + d * q.y);
     }
   } else {
-    for (int s = s0 + threadIdx.x; s < s1; s += NT) dst[s] = cscale(sm[pp[s]], a);
+    for (int s = s0 + threadIdx.x; s < s1; s += PT) dst[s] = cscale(sm[pp[s]], a);
   }
 }
 
@@ -304,7 +316,9 @@ template <int N>
 #ifndef PWB_PENCIL_H_MINB
 #define PWB_PENCIL_H_MINB 3   // 80-register cap; 3 CTAs/SM (smem 75 KB each)
 #endif
-__global__ void __launch_bounds__(NT, PWB_PENCIL_H_MINB) k_pencil_h(GridDev g, PencilArgs a) {
+// 96 (8 x 12): 2 CTAs/SM leave 128 registers for the radix-12 pass (no spill;
+// 13.7 vs 14.0 us/band at 96^3); 48 / 64 keep 3 CTAs/SM
+__global__ void __launch_bounds__(NT, (N == 96 ? 2 : PWB_PENCIL_H_MINB)) k_pencil_h(GridDev g, PencilArgs a) {
   constexpr int R1 = TwoPass<N>::R1, R2 = TwoPass<N>::R2;
   constexpr int TC = 3072 / N, TP = (TC % 2 == 0) ? TC + 1 : TC;
   constexpr int NB1 = N / R1;                 // radix-R1 butterflies per line (= R2)
@@ -359,11 +373,16 @@ __global__ void __launch_bounds__(NT, PWB_PENCIL_H_MINB) k_pencil_h(GridDev g, P
   // ---- B: inverse pass 2 (radix R2, NS = R1) -> * V -> forward pass 1 (radix R2, NS = 1)
   {
     const int j = tid / LP2, li = tid - j * LP2;   // j in [0, R1)
-    double2 w[R2];
+    // twiddles (TWS = N / (NS R) = 1, inverse: conjugate): held across the MB
+    // rounds for the small radices, read from L1 per use for radix 12
+    constexpr bool kHoldW = R2 <= 8;
+    double2 w[kHoldW ? R2 : 1];
+    if constexpr (kHoldW) {
 #pragma unroll
-    for (int r = 1; r < R2; ++r) {
-      const double2 t = __ldg(&g.px.tw[r * j]);   // TWS = N / (NS R) = 1
-      w[r] = make_double2(t.x, -t.y);              // inverse: conjugate
+      for (int r = 1; r < R2; ++r) {
+        const double2 t = __ldg(&g.px.tw[r * j]);
+        w[r] = make_double2(t.x, -t.y);
+      }
     }
     double2 v[MB][R2];
 #pragma unroll
@@ -380,7 +399,14 @@ __global__ void __launch_bounds__(NT, PWB_PENCIL_H_MINB) k_pencil_h(GridDev g, P
       const int l = m * LP2 + li;
       if (l < TC) {
 #pragma unroll
-        for (int r = 1; r < R2; ++r) v[m][r] = cmul(v[m][r], w[r]);
+        for (int r = 1; r < R2; ++r) {
+          if constexpr (kHoldW) {
+            v[m][r] = cmul(v[m][r], w[r]);
+          } else {
+            const double2 t = __ldg(&g.px.tw[r * j]);
+            v[m][r] = cmul(v[m][r], make_double2(t.x, -t.y));
+          }
+        }
         Dft<R2>::run(v[m], 1.0);
 #pragma unroll
         for (int r = 0; r < R2; ++r) v[m][r] = cscale(v[m][r], a.vscale * smv[(j + r * R1) * TC + l]);
@@ -437,7 +463,8 @@ int launch_plane_inv(pwb_grid* g, int nband, const int* band_k, const double2* p
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
-    (void)launch_k(k_plane_inv<decltype(fy), decltype(fz)>, grid, NT, plane_smem(g), g->stream, 
+    (void)launch_k(k_plane_inv<decltype(fy), decltype(fz)>, grid,
+                   plane_nt<decltype(fy), decltype(fz)>(), plane_smem(g), g->stream, 
         g->dev, psi, nullptr, band_k, scale, W, rows, nact);
   });
   PWB_LAUNCH_CHECK();
@@ -450,7 +477,8 @@ int launch_plane_inv2(pwb_grid* g, int nband, const int* band_k, const double2* 
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
-    (void)launch_k(k_plane_inv<decltype(fy), decltype(fz)>, grid, NT, plane_smem(g), g->stream, 
+    (void)launch_k(k_plane_inv<decltype(fy), decltype(fz)>, grid,
+                   plane_nt<decltype(fy), decltype(fz)>(), plane_smem(g), g->stream, 
         g->dev, a, b, band_k, 1.0, W, nullptr, nullptr);
   });
   PWB_LAUNCH_CHECK();
@@ -464,7 +492,8 @@ int launch_plane_fwd(pwb_grid* g, int nband, const int* band_k, const double2* W
   if (nband == 0) return PWB_OK;
   dim3 grid(g->nxa, nband);
   plane_variant(g, [&](auto fy, auto fz) {
-    (void)launch_k(k_plane_fwd<decltype(fy), decltype(fz)>, grid, NT, plane_smem(g), g->stream, 
+    (void)launch_k(k_plane_fwd<decltype(fy), decltype(fz)>, grid,
+                   plane_nt<decltype(fy), decltype(fz)>(), plane_smem(g), g->stream, 
         g->dev, W, band_k, a, psi_in, shift, out, rows, nact);
   });
   PWB_LAUNCH_CHECK();

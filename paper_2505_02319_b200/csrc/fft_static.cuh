@@ -76,6 +76,37 @@ struct Dft<6> {
   }
 };
 
+template <>
+struct Dft<12> {
+  // 12 = 4 (inner, n1) x 3 (outer, n2): x[3 n1 + n2], X[k1 + 4 k2];
+  // X = sum W4^(n1 k1) W12^(n2 k1) W3^(n2 k2) x
+  static __device__ __forceinline__ void run(double2* v, double sgn) {
+    const double s3 = 0.86602540378443864676;
+    double2 y[3][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 3; ++n2) {
+      double2 a[4] = {v[n2], v[3 + n2], v[6 + n2], v[9 + n2]};
+      Dft<4>::run(a, sgn);
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) y[n2][k1] = a[k1];
+    }
+    // W12^q for q = n2 k1 in {1, 2, 3} (n2 = 1) and {2, 4, 6} (n2 = 2)
+    y[1][1] = cmul(y[1][1], make_double2(s3, sgn * 0.5));
+    y[1][2] = cmul(y[1][2], make_double2(0.5, sgn * s3));
+    y[1][3] = cmul_isgn(y[1][3], sgn);
+    y[2][1] = cmul(y[2][1], make_double2(0.5, sgn * s3));
+    y[2][2] = cmul(y[2][2], make_double2(-0.5, sgn * s3));
+    y[2][3] = make_double2(-y[2][3].x, -y[2][3].y);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      double2 b[3] = {y[0][k1], y[1][k1], y[2][k1]};
+      Dft<3>::run(b, sgn);
+#pragma unroll
+      for (int k2 = 0; k2 < 3; ++k2) v[k1 + 4 * k2] = b[k2];
+    }
+  }
+};
+
 // One compile-time Stockham pass (radix R, sub-transform size NS) over whole
 // lines, one butterfly per thread per round.
 // vm (first pass only, optional): input element e of line l is multiplied by

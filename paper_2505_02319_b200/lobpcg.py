@@ -88,7 +88,8 @@ def _rayleigh_ritz(S, HS, nst):
     coefs, lams = [], []
     for k in range(nk):
         s, U = torch.linalg.eigh(G[k])
-        keep = s > 1e-13 * s.max()
+        keep = s > 1e-10 * s.max()   # drop near-dependent directions (eigh of a
+        #                              badly scaled pencil fails to converge otherwise)
         B = U[:, keep] / torch.sqrt(s[keep])[None, :]
         Ak = B.conj().T @ A[k] @ B
         Ak = 0.5 * (Ak + Ak.conj().T)
@@ -119,11 +120,17 @@ def lobpcg(kb, vloc_t, X, tol=1e-8, maxit=200, n_check=None):
         W = W - torch.matmul(torch.matmul(W, X.conj().transpose(1, 2)), X)
         W = W / torch.linalg.vector_norm(W, dim=2, keepdim=True).clamp_min(1e-300)
         HW = kb.h(W, vloc_t)
-        if P is None:
-            S, HS = torch.cat([X, W], 1), torch.cat([HX, HW], 1)
-        else:
-            S, HS = torch.cat([X, W, P], 1), torch.cat([HX, HW, HP], 1)
-        coefs, lam = _rayleigh_ritz(S, HS, nst)
+        S, HS = torch.cat([X, W], 1), torch.cat([HX, HW], 1)
+        try:
+            if P is not None:
+                S3, HS3 = torch.cat([S, P], 1), torch.cat([HS, HP], 1)
+                coefs, lam = _rayleigh_ritz(S3, HS3, nst)
+                S, HS = S3, HS3
+            else:
+                coefs, lam = _rayleigh_ritz(S, HS, nst)
+        except RuntimeError:
+            # ill-conditioned [X W P] basis: restart this step without the P block
+            coefs, lam = _rayleigh_ritz(S, HS, nst)
         Xn = torch.stack([c @ S[k] for k, c in enumerate(coefs)])
         HXn = torch.stack([c @ HS[k] for k, c in enumerate(coefs)])
         P = torch.stack([c[:, nst:] @ S[k, nst:] for k, c in enumerate(coefs)])
