@@ -76,10 +76,15 @@ __global__ void __launch_bounds__(NTC) k_cg_init(GridDev g, CgScalars sc, int n,
 __global__ void __launch_bounds__(NTC) k_cg_init2(GridDev g, CgScalars sc, int n,
                                                   const double2* __restrict__ xr,
                                                   const double2* __restrict__ z,
-                                                  double2* __restrict__ p) {
+                                                  double2* __restrict__ p, int* __restrict__ hdr,
+                                                  int cap) {
   pdl_wait();
   __shared__ double red[NTC / 32 + 1];
   const int row = blockIdx.x;
+  if (row == 0 && threadIdx.x == 0) {   // device-side iteration loop: counter and cap
+    hdr[5] = 0;
+    hdr[6] = cap;
+  }
   const double2* r = xr + (size_t)(n + row) * g.nbp;
   const double2* zz = z + (size_t)row * g.nbp;
   double2* pp = p + (size_t)row * g.nbp;
@@ -269,6 +274,14 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
   }
 }
 
+// End of one device-side CG iteration: keep looping while any row still
+// iterates (k_cg_resid's count) and the safety cap is not reached.
+__global__ void k_loop_ctl(cudaGraphConditionalHandle h, int* __restrict__ hdr) {
+  pdl_wait();
+  const int n = ++hdr[5];
+  cudaGraphSetConditional(h, (hdr[3] > 0 && n < hdr[6]) ? 1u : 0u);
+}
+
 CgBatch::~CgBatch() {
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
@@ -386,7 +399,7 @@ int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands) {
 }
 
 // Enqueue one CG iteration on stream s (direct launches or graph capture).
-static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s) {
+static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s, bool readback = true) {
   pwb_grid* g = st->g;
   const int n = cg.nrows;
   double2* xr = as<double2>(cg.xr);
@@ -427,7 +440,7 @@ static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s) {
     (void)launch_k(k_cg_resid, n, NTC, 0, s, g->dev, cg.s, n, xr, z, rows, nact, cg.ctl.hdr + 3);
     count_launch();
     prof().end(PROF_CG, ec, s, cg.prof_rows);
-    cudaMemcpyAsync(cg.h_hdr, cg.ctl.hdr, 8 * sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (readback) cudaMemcpyAsync(cg.h_hdr, cg.ctl.hdr, 8 * sizeof(int), cudaMemcpyDeviceToHost, s);
     if ((status = project_rows(st, cg.pa, z, cg.s.active, n, rows, part, cmat, s, cg.ctl.hdr + 1)))
       break;
     ec = prof().begin(s);
@@ -445,8 +458,62 @@ static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s) {
 // launches of one iteration (for the gpu_launches count when replaying the graph)
 static unsigned long long g_iter_launches = 0;
 
+// The whole CG loop as ONE graph: a WHILE conditional node whose body is one
+// iteration plus k_loop_ctl (no host round trip per iteration).  Returns false
+// (nothing built, errors cleared) when the driver refuses it.
+static bool build_loop_graph(pwb_state* st, CgBatch& cg) {
+  static const bool disabled = getenv("PWB_NO_DEVLOOP") != nullptr;   // A/B measurement
+  if (disabled) return false;
+  cudaStream_t cs = cg.graph_stream;
+  const unsigned long long before = g_launches;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool ok = cudaGraphCreate(&graph, 0) == cudaSuccess;
+  cudaGraphConditionalHandle h{};
+  cudaGraph_t body = nullptr;
+  if (ok) ok = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault) ==
+               cudaSuccess;
+  if (ok) {
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    ok = cudaGraphAddNode(&node, graph, nullptr, 0, &np) == cudaSuccess;
+    if (ok) body = np.conditional.phGraph_out[0];
+  }
+  if (ok) ok = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    int status = enqueue_iteration(st, cg, cs, false);
+    if (status == PWB_OK) {
+      (void)launch_k(k_loop_ctl, 1, 1, 0, cs, h, cg.ctl.hdr);
+      count_launch();
+    }
+    cudaGraph_t captured = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(cs, &captured);
+    ok = status == PWB_OK && e == cudaSuccess;
+  }
+  if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+  g_iter_launches = g_launches - before;
+  g_launches = before;   // nothing ran during capture
+  if (!ok) {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    (void)cudaGetLastError();
+    return false;
+  }
+  cg.graph = graph;
+  cg.exec = exec;
+  cg.loop_graph = true;
+  return true;
+}
+
 static int ensure_graph(pwb_state* st, CgBatch& cg) {
   if (cg.exec) return PWB_OK;
+  if (build_loop_graph(st, cg)) return PWB_OK;
+  cg.loop_graph = false;
   cudaStream_t cs = cg.graph_stream;
   const unsigned long long before = g_launches;
   PWB_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
@@ -484,7 +551,9 @@ int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max
   PWB_LAUNCH_CHECK();
   PWB_TRY(project_rows(st, cg.plan1, z, nullptr, n, nullptr, as<double2>(cg.part),
                        as<double2>(cg.cmat), s, nullptr));
-  (void)launch_k(k_cg_init2, n, NTC, 0, s, g->dev, cg.s, n, xr, z, p);
+  int cap = 0;
+  for (int m : maxit) cap = std::max(cap, m);
+  (void)launch_k(k_cg_init2, n, NTC, 0, s, g->dev, cg.s, n, xr, z, p, cg.ctl.hdr, cap + 2);
   PWB_LAUNCH_CHECK();
   const size_t wbytes = (size_t)n * g->nxa * g->nyz * sizeof(double2);
   if (g->wbuf.bytes < wbytes || !g->wbuf.ptr) {
@@ -502,7 +571,14 @@ int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max
     cg.graph_w = g->wbuf.ptr;
   }
   cg.prof_rows = n;   // rows active in the next iteration (profiling units only)
-  for (;;) {
+  if (use_graph && cg.loop_graph) {   // the whole loop on the device
+    PWB_CUDA(cudaGraphLaunch(cg.exec, s));
+    PWB_CUDA(cudaMemcpyAsync(cg.h_hdr, cg.ctl.hdr, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    PWB_CUDA(cudaStreamSynchronize(s));
+    count_launch((int)(g_iter_launches * (unsigned long long)std::max(cg.h_hdr[5], 1)));
+    if (cg.h_hdr[3] != 0) return fail(PWB_ERR_NONCONV, "Sternheimer CG: iteration cap reached");
+  }
+  for (; !(use_graph && cg.loop_graph);) {
     if (use_graph) {
       PWB_CUDA(cudaGraphLaunch(cg.exec, s));
       count_launch((int)g_iter_launches);

@@ -49,6 +49,7 @@ struct CgBatch {
   cudaGraphExec_t exec = nullptr;
   cudaStream_t graph_stream = nullptr;
   void* graph_w = nullptr;  // plane buffer captured in the graph
+  bool loop_graph = false;  // graph = WHILE conditional node around one iteration
   int prof_rows = 0;        // active rows of the running iteration (profiler units)
   ~CgBatch();
 };
