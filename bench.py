@@ -52,9 +52,15 @@ def parse():
 
 
 def dist_env():
+    """(world, rank, local device).  PWB_SHARE_GPU=1 (control-flow check of the
+    sharded path on a one-GPU box, never a measurement) maps every rank to the
+    visible devices round-robin."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PWB_SHARE_GPU"):
+        import torch
+        local %= max(1, torch.cuda.device_count())
     return world, rank, local
 
 
@@ -556,7 +562,9 @@ def main():
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PWB_DIST_BACKEND", "nccl")   # gloo: the shared-GPU check
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)}
+                                            if backend == "nccl" else {}))
         group = dist.group.WORLD
     from paper_2505_02319_b200 import _lib
     from paper_2505_02319_b200.device import device_state

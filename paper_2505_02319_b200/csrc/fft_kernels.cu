@@ -12,6 +12,7 @@
 // plane buffer ("Kernels").  Only nxa of nx planes (the sphere
 // occupies |ix| <= ~N/4 of the 2x-oversampled cube) are ever stored.
 #include "dispatch.cuh"
+#include "tma.cuh"
 
 namespace pwb {
 
@@ -443,6 +444,162 @@ __global__ void __launch_bounds__(NT, (N == 96 ? 2 : PWB_PENCIL_H_MINB)) k_penci
   }
 }
 
+// ----------------------------------------------------------------------------
+// Pipelined H-apply pencil: the same three passes as k_pencil_h, but each CTA is
+// persistent over a contiguous range of (band, tile) items and a producer warp
+// streams the NEXT items' active W rows into a ring of shared-memory stages with
+// TMA bulk copies (one copy per active x row, completion on an mbarrier), so the
+// HBM reads of item n+1 overlap the FFTs of item n.  ncu on k_pencil_h (48^3):
+// the top stall was pass A waiting on its global loads (long scoreboard) at
+// ~1.9 TB/s.  V(r) is read from L2 in pass B (x-major, coalesced) to leave the
+// shared memory for the stages: 2 CTAs of 9 warps per SM.
+constexpr int kHpStages = 2;
+
+template <int N>
+struct PencilHp {
+  static constexpr int TC = 3072 / N, TP = (TC % 2 == 0) ? TC + 1 : TC;
+  // double2 elements: work area, then kHpStages stages of nxa x TC
+  static size_t smem(int nxa) {
+    return ((size_t)N * TP + (size_t)kHpStages * nxa * TC) * 16 + 2 * kHpStages * 8 + 16;
+  }
+};
+
+template <int N>
+__global__ void __launch_bounds__(NT + 32, 2) k_pencil_hp(GridDev g, PencilArgs a, int nb_host,
+                                                          int ntiles) {
+  constexpr int R1 = TwoPass<N>::R1, R2 = TwoPass<N>::R2;
+  constexpr int TC = PencilHp<N>::TC, TP = PencilHp<N>::TP;
+  constexpr int NB1 = N / R1;
+  constexpr int LP1 = NT / NB1;
+  constexpr int LP2 = NT / R1;
+  constexpr int MB = (TC + LP2 - 1) / LP2;
+  constexpr int NW = NT / 32;
+  static_assert(NB1 == R2, "two-pass plan");
+  pdl_wait();
+  extern __shared__ __align__(128) double2 sm[];
+  const int nxa = a.nxin;
+  double2* stages = sm + N * TP;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)kHpStages * nxa * TC);
+  uint64_t* empty = full + kHpStages;
+  const int nyz = g.nyz;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int nb = a.nact ? *a.nact : nb_host;
+  const int nitems = nb * ntiles;   // item = band * ntiles + tile
+  const int per = (nitems + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * per, i1 = min(nitems, i0 + per);
+  if (tid == 0) {
+    for (int s = 0; s < kHpStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (w == NW) {   // producer warp
+    for (int item = i0, n = 0; item < i1; ++item, ++n) {
+      const int s = n % kHpStages;
+      if (n >= kHpStages) mbar_wait(&empty[s], ((n / kHpStages) + 1) & 1);
+      const int b = item / ntiles, t0 = (item - b * ntiles) * TC;
+      const int nt = min(TC, nyz - t0);
+      if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(nxa * nt * 16));
+      __syncwarp();
+      const double2* src = a.win + (size_t)b * a.in_stride + t0;
+      double2* dst = stages + (size_t)s * nxa * TC;
+      for (int p = lane; p < nxa; p += 32)
+        bulk_g2s(dst + p * TC, src + (size_t)p * nyz, (uint32_t)(nt * 16), &full[s]);
+    }
+    return;
+  }
+  const int x0 = a.xin[0];
+  for (int item = i0, n = 0; item < i1; ++item, ++n) {
+    const int s = n % kHpStages;
+    const int b = item / ntiles, t0 = (item - b * ntiles) * TC;
+    const int nt = min(TC, nyz - t0);
+    const double2* st = stages + (size_t)s * nxa * TC;
+    mbar_wait(&full[s], (n / kHpStages) & 1);
+    // ---- A: inverse pass 1 (radix R1, NS = 1) from the stage
+    {
+      const int j = tid / LP1, li = tid - j * LP1;
+      if (j < NB1) {
+        for (int l = li; l < TC; l += LP1) {
+          double2 v[R1];
+#pragma unroll
+          for (int r = 0; r < R1; ++r) {
+            int p = j + r * NB1 - x0;
+            if (p < 0) p += N;
+            v[r] = (p < nxa && l < nt) ? st[p * TC + l] : make_double2(0.0, 0.0);
+          }
+          Dft<R1>::run(v, 1.0);
+#pragma unroll
+          for (int r = 0; r < R1; ++r) sm[(j * R1 + r) * TP + l] = v[r];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+    // ---- B: inverse pass 2 -> * V (from L2) -> forward pass 1, in registers
+    {
+      const int j = tid / LP2, li = tid - j * LP2;
+      double2 v[MB][R2];
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        const int l = m * LP2 + li;
+        if (l < TC) {
+#pragma unroll
+          for (int r = 0; r < R2; ++r) v[m][r] = sm[(j + r * R1) * TP + l];
+        }
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        const int l = m * LP2 + li;
+        if (l < TC) {
+#pragma unroll
+          for (int r = 1; r < R2; ++r) {
+            const double2 t = __ldg(&g.px.tw[r * j]);   // inverse: conjugate
+            v[m][r] = cmul(v[m][r], make_double2(t.x, -t.y));
+          }
+          Dft<R2>::run(v[m], 1.0);
+#pragma unroll
+          for (int r = 0; r < R2; ++r) {
+            const double vv = l < nt ? __ldg(&a.v[(size_t)(j + r * R1) * nyz + t0 + l]) : 0.0;
+            v[m][r] = cscale(v[m][r], a.vscale * vv);
+          }
+          Dft<R2>::run(v[m], -1.0);
+#pragma unroll
+          for (int r = 0; r < R2; ++r) sm[(j * R2 + r) * TP + l] = v[m][r];
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+    // ---- C: forward pass 2 (radix R1, NS = R2) -> active rows to global
+    {
+      const int j = tid / LP1, li = tid - j * LP1;
+      if (j < NB1) {
+        double2* dst = a.wout + (size_t)b * a.out_stride;
+        for (int l = li; l < TC; l += LP1) {
+          double2 v[R1];
+#pragma unroll
+          for (int r = 0; r < R1; ++r) v[r] = sm[(j + r * R2) * TP + l];
+#pragma unroll
+          for (int r = 1; r < R1; ++r) v[r] = cmul(v[r], __ldg(&g.px.tw[r * j]));
+          Dft<R1>::run(v, -1.0);
+          if (l < nt) {
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+              int p = j + r * R2 - x0;
+              if (p < 0) p += N;
+              if (p < nxa) dst[(size_t)p * nyz + t0 + l] = cscale(v[r], a.oscale);
+            }
+          }
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");   // work area reused next item
+  }
+}
+
 size_t plane_smem(const pwb_grid* g) { return (size_t)g->nz * g->dev.nyp * sizeof(double2); }
 size_t pencil_smem(const pwb_grid* g) { return (size_t)g->nx * g->dev.tilep * sizeof(double2); }
 // W -> W pencil with the V(r) multiply: + the tile's V values (x-major doubles)
@@ -553,10 +710,18 @@ int launch_pencil_vmul(pwb_grid* g, int nband, double2* W, const double* v, doub
   a.out_stride = a.in_stride;
   dim3 grid(tiles(g), nband);
   static const bool generic_only = getenv("PWB_NO_PENCIL_H") != nullptr;   // A/B measurement
+  static const bool no_hp = getenv("PWB_NO_PENCIL_HP") != nullptr;          // A/B measurement
   pencil_variant(g, [&](auto fx) {
     using FX = decltype(fx);
     constexpr int TC = FX::N ? 3072 / FX::N : 0;
     if constexpr (TwoPass<FX::N>::ok) {
+      if (!generic_only && !no_hp && g->dev.tile == TC) {
+        const int nt = tiles(g);
+        const int gsz = (int)std::min<long>((long)nt * nband, 2L * kSM);
+        (void)launch_k(k_pencil_hp<FX::N>, gsz, NT + 32, PencilHp<FX::N>::smem(g->nxa), g->stream,
+                       g->dev, a, nband, nt);
+        return;
+      }
       if (!generic_only && g->dev.tile == TC) {
         (void)launch_k(k_pencil_h<FX::N>, grid, NT, pencil_smem_v(g), g->stream, g->dev, a);
         return;
@@ -727,6 +892,9 @@ int configure_kernels(const pwb_grid* g) {
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_pencil_h<FX::N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pencil_smem_v(g));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_pencil_hp<FX::N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)PencilHp<FX::N>::smem(g->nxa));
     }
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_pencil<0, 1, FX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);

@@ -28,9 +28,13 @@
 #include <cstring>
 
 #include "proj.cuh"
+#include "tma.cuh"
 
 namespace pwb {
 
+#ifndef PWB_RED_W
+#define PWB_RED_W 1   // modelled cost of one split in the last CTA's sum (1/16 chunk units)
+#endif
 constexpr int TR = kProjTileRows;   // rows per tile (<= 2 DMMA n-fragments)
 constexpr int KC = kProjChunk;      // sphere coefficients per pipeline chunk
 constexpr int MF = 5;               // m fragments per block
@@ -50,35 +54,6 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P1;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @P1 bra DONE_%=;\n"
-      " bra WAIT_%=;\n"
-      "DONE_%=:\n}\n" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
-          "r"(su32(dst)),
-      "l"(src), "r"(bytes), "r"(su32(b))
-      : "memory");
-}
 __device__ __forceinline__ int xrow(const ProjArgs& a, const ProjTile& t, int r) {
   return a.rows ? a.rows[t.row0 + r] : t.row0 + r;
 }
@@ -110,7 +85,7 @@ __device__ __forceinline__ CoefGeom coef_geom(const ProjArgs& a, int nt_host, in
     const int sc = (g.nchunk + s - 1) / s;
     if ((g.nchunk + sc - 1) / sc != s) continue;   // only exact split counts
     const unsigned long long busiest =
-        (unsigned long long)((units * s + grid - 1) / grid) * (sc + 1) * 16 + s;
+        (unsigned long long)((units * s + grid - 1) / grid) * (sc + 1) * 16 + PWB_RED_W * s;
     best = min(best, (busiest << 16) | (unsigned)s);   // ties -> fewer splits
   }
 #pragma unroll
@@ -168,9 +143,6 @@ struct CoefCursor {
   }
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
-}
 // barrier among the NW consumer warps only (the producer warp runs free)
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(NW * 32) : "memory");
