@@ -79,13 +79,17 @@ __device__ __forceinline__ CoefGeom coef_geom(const ProjArgs& a, int nt_host, in
   g.nchunk = a.nbp / KC;
   const int units = max(1, g.ntiles * mtiles);
   const int lane = threadIdx.x & 31, grid = gridDim.x;
+  // entries of one tile's C block: the last CTA's s-way sum costs ~ s E / 132
+  // sixteenths of a chunk (qbench at 1..522 rows; 16 rows x 33 orbitals -> 4 s)
+  const int E = (g.ntiles == 1 ? a.tiles[0].nrows : TR) * min(CM, a.ldc);
+  const int rw = max(PWB_RED_W, E / 132);
   smax = min(smax, g.nchunk);
   unsigned long long best = ~0ull;
   for (int s = lane + 1; s <= smax; s += 32) {
     const int sc = (g.nchunk + s - 1) / s;
     if ((g.nchunk + sc - 1) / sc != s) continue;   // only exact split counts
     const unsigned long long busiest =
-        (unsigned long long)((units * s + grid - 1) / grid) * (sc + 1) * 16 + PWB_RED_W * s;
+        (unsigned long long)((units * s + grid - 1) / grid) * (sc + 1) * 16 + rw * s;
     best = min(best, (busiest << 16) | (unsigned)s);   // ties -> fewer splits
   }
 #pragma unroll
@@ -157,9 +161,10 @@ __device__ __forceinline__ const double2* phic_at(const ProjArgs& a, int k, int 
 // Producer warp (warp NW) of the coef kernel: walks the same (item, chunk)
 // sequence as the consumers and keeps SCC stages in flight.  The chunk's Phi
 // block is ONE contiguous TMA bulk copy (chunk-major layout); the up to 16
-// gathered X rows (1 KB each) go by cp.async from all 32 lanes, completing on
-// the same mbarrier (cp.async.mbarrier.arrive.noinc: 1 + 32 arrivals).  Sixteen
-// small bulk copies cost ~0.4 us more per stage than one (tools/tma_bw.cu).
+// gathered X rows (1 KB each) are one bulk copy per row issued by lanes
+// 0..15, all completing on the stage's mbarrier (one expect_tx arrival).
+// (The cp.async 16-byte gather, -DPWB_COEF_CPASYNC, left the consumers
+// waiting on the full barrier: 8% slower at 261-522 rows, tools/qbench.py.)
 // Row sources are resolved once per item.
 __device__ void coef_producer(const ProjArgs& a, const CoefGeom& g, const double2* X,
                               double2* stages, uint64_t* full, uint64_t* empty, int lane) {
@@ -177,12 +182,23 @@ __device__ void coef_producer(const ProjArgs& a, const CoefGeom& g, const double
       xsrc = lane < nrows ? X + (size_t)xrow(a, c.it.t, lane) * a.nbp : nullptr;
     }
     double2* buf = stages + s * kCoefStage;
+    const size_t g0 = (size_t)c.chunk * KC;
+#ifndef PWB_COEF_CPASYNC
+    if (lane == 0) {   // one arrival: expected bytes of the Phi block and the X rows
+      const uint32_t bytes = (uint32_t)c.it.nm * RSC * 16;
+      mbar_expect_tx(&full[s], bytes + (uint32_t)nrows * KC * 16);
+      bulk_g2s(buf + TR * RSC, phic_at(a, c.it.t.k, nocc, c.chunk, c.it.m0), bytes, &full[s]);
+    }
+    __syncwarp();
+    if (lane < nrows) bulk_g2s(buf + lane * RSC, xsrc + g0, KC * 16, &full[s]);
+    c.next(a, g);
+    continue;
+#endif
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)c.it.nm * RSC * 16;
       mbar_expect_tx(&full[s], bytes);
       bulk_g2s(buf + TR * RSC, phic_at(a, c.it.t.k, nocc, c.chunk, c.it.m0), bytes, &full[s]);
     }
-    const size_t g0 = (size_t)c.chunk * KC;
     for (int p = lane; p < nrows * KC; p += 32) {   // 16-byte pieces, row r = p / KC
       const int r = p / KC, o = p - r * KC;
       const double2* src = reinterpret_cast<const double2*>(
@@ -214,7 +230,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   const size_t stride = (size_t)tile_cap * mtiles * (CM * TR);   // partials per split
   if (threadIdx.x == 0) {
     for (int s = 0; s < SCC; ++s) {
+#ifndef PWB_COEF_CPASYNC
+      mbar_init(&full[s], 1);        // one expect_tx arrival (all bulk copies)
+#else
       mbar_init(&full[s], 1 + 32);   // TMA expect_tx arrival + 32 cp.async lanes
+#endif
       mbar_init(&empty[s], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
