@@ -30,6 +30,14 @@ from .strategies import StrategySpec, parse_strategy, tolerances_k
 TIGHT_CG_TOL = 1e-16
 
 
+@dataclass(frozen=True)
+class Perturbation:
+    """Gaussian-displacement perturbation (reference config.py:23-27)."""
+    gaussian: int = 0
+    direction: tuple = (1.0, 0.0, 0.0)
+    analytic: bool = True
+
+
 @dataclass
 class DysonResult:
     solution: object
@@ -47,6 +55,9 @@ class DysonResult:
     wall_s: float = 0.0
     final_true_res: float = np.nan
     eta: float = np.nan
+    y_final: object = None          # last cycle's least-squares coefficients (igmres.py:154)
+    cycle_est_res: list = field(default_factory=list)
+    sigma_final: float = np.nan
 
 
 def row_norms(gs):
@@ -147,7 +158,8 @@ def solve_dyson(gs, dv0, strategy="bal", tau=1e-8, m=10, xc=None, kerker_alpha=0
                       n_ham=n_ham, n_ham_rhs=n_rhs, final_est_res=rep.final_est_res,
                       est_res_history=list(rep.est_res_history), tolerance_schedule=sched,
                       cg_iterations=cgits, budgets=list(rep.budgets),
-                      restarts=list(rep.restarts), wall_s=wall)
+                      restarts=list(rep.restarts), wall_s=wall, y_final=rep.y_final,
+                      cycle_est_res=list(rep.cycle_est_res), sigma_final=rep.sigma_final)
     if with_true_residual:
         res.final_true_res = true_residual(gs, kernel, rep.solution, b_t)
         if n_ham > 0 and res.final_true_res > 0 and b_norm > 0:
