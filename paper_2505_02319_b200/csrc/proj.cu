@@ -557,11 +557,278 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Fused small-batch projector: Q X in ONE launch for a few tiles of one orbital
+// block (N_occ <= CM).  CTA (tile t, split j) owns chunks [c0, c1) of tile t:
+//   1. one TMA burst brings the X rows and the Phi blocks of ALL its chunks
+//      into smem (<= kSmallChunks stages), partial C over them (DMMA, the
+//      coef kernel's fragment code), fixed-order warp reduction -> partials;
+//   2. the last CTA of tile t to arrive sums the s partials in split order,
+//      writes C and bumps the tile's generation flag; the others spin on it
+//      (all CTAs are co-resident: grid <= #SM, one CTA per SM by smem);
+//   3. every CTA applies Y = X - Phi C on its chunks from the SAME smem copies
+//      (no second launch, no reload of X or Phi).
+// Latency chain of the two-kernel path at 1-16 rows (~17-24 us per Q:
+// two launches, two TMA fills, last-CTA sum, PDL hand-over) -> one launch.
+constexpr int kSmallChunks = 3;
+constexpr size_t kSmallSmem = (size_t)kSmallChunks * kCoefStage * 16 + (size_t)(NW / 2) * CM * TR * 16 + 64;
+static_assert(kSmallSmem <= 232448, "small projector smem");
+
+struct SmallGeom {
+  int ntiles, s, sc;
+};
+__device__ __forceinline__ SmallGeom small_geom(int ntiles, int nchunk) {
+  SmallGeom g;
+  // as few splits as the smem allows: the split-order sum is the latency
+  g.ntiles = ntiles;
+  g.sc = kSmallChunks;
+  g.s = (nchunk + g.sc - 1) / g.sc;
+  return g;
+}
+
+__global__ void __launch_bounds__(NW * 32, 1)
+    k_proj_small(ProjArgs a, double2* __restrict__ X, const int* __restrict__ active,
+                 int band_mod, double2* __restrict__ part, double2* __restrict__ C,
+                 unsigned* __restrict__ counters, unsigned* __restrict__ flags, int nt_host) {
+  pdl_wait();
+  extern __shared__ __align__(128) double2 sm[];
+  double2* red = sm + kSmallChunks * kCoefStage;   // [NW/2][CM][TR]; later C tile [TR][CM+4]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + (NW / 2) * CM * TR);
+  __shared__ bool last;
+  __shared__ unsigned gen0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r4 = lane >> 2, c4 = lane & 3;
+  const int ntiles = a.ntiles ? *a.ntiles : nt_host;
+  const int nchunk = a.nbp / KC;
+  const SmallGeom gg = small_geom(ntiles, nchunk);
+  const int tile = blockIdx.x / gg.s, split = blockIdx.x - tile * gg.s;
+  if (tile >= ntiles || gg.sc > kSmallChunks) return;   // (host guarantees sc fits)
+  const ProjTile t = a.tiles[tile];
+  const int nocc = a.nocc[t.k];
+  const int c0 = split * gg.sc, c1 = min(nchunk, c0 + gg.sc), nc = c1 - c0;
+  const int nrows = t.nrows;
+  if (threadIdx.x == 0) {
+    gen0 = *((volatile unsigned*)&flags[tile]);
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // ---- 1. all chunks of this CTA in one TMA burst
+  if (w == 0) {
+    const uint32_t pb = (uint32_t)nocc * RSC * 16;
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)nc * (pb + (uint32_t)nrows * KC * 16));
+    __syncwarp();
+    for (int c = 0; c < nc; ++c) {
+      double2* buf = sm + c * kCoefStage;
+      if (lane == 0) bulk_g2s(buf + TR * RSC, phic_at(a, t.k, nocc, c0 + c, 0), pb, bar);
+      if (lane < nrows)
+        bulk_g2s(buf + lane * RSC, X + (size_t)xrow(a, t, lane) * a.nbp + (size_t)(c0 + c) * KC,
+                 KC * 16, bar);
+    }
+  }
+  // zero the unused tails of the stages (rows >= nrows, orbitals >= nocc) are
+  // never read: the fragment predicates below bound rows / orbitals
+  mbar_wait(bar, 0);
+  const int nfm = (nocc + 7) >> 3, nfn = (nrows + 7) >> 3;
+  double t1[MF][2][2], t2[MF][2][2], t3[MF][2][2];
+#pragma unroll
+  for (int ma = 0; ma < MF; ++ma)
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      t1[ma][nb][0] = t1[ma][nb][1] = 0.0;
+      t2[ma][nb][0] = t2[ma][nb][1] = 0.0;
+      t3[ma][nb][0] = t3[ma][nb][1] = 0.0;
+    }
+  for (int c = 0; c < nc; ++c) {
+    const double2* xs = sm + c * kCoefStage;
+    const double2* ps = xs + TR * RSC;
+#pragma unroll
+    for (int kk = 0; kk < KC / (4 * NW); ++kk) {
+      const int gl = 4 * (w + NW * kk) + c4;
+      double2 bv[2];
+      double bs[2];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        bv[nb] = (nb < nfn && 8 * nb + r4 < nrows) ? xs[(8 * nb + r4) * RSC + gl]
+                                                    : make_double2(0.0, 0.0);
+        bs[nb] = bv[nb].x + bv[nb].y;
+      }
+#pragma unroll
+      for (int ma = 0; ma < MF; ++ma) {
+        if (ma >= nfm) break;
+        const double2 av = (8 * ma + r4 < nocc) ? ps[(8 * ma + r4) * RSC + gl]
+                                                 : make_double2(0.0, 0.0);
+        const double ad = av.x - av.y;
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+          if (nb >= nfn) break;
+          dmma(t1[ma][nb][0], t1[ma][nb][1], av.x, bv[nb].x);
+          dmma(t2[ma][nb][0], t2[ma][nb][1], av.y, bv[nb].y);
+          dmma(t3[ma][nb][0], t3[ma][nb][1], ad, bs[nb]);
+        }
+      }
+    }
+  }
+  // fixed-order warp reduction (as in k_proj_coef)
+  if (w >= NW / 2) {
+#pragma unroll
+    for (int ma = 0; ma < MF; ++ma)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          red[((w - NW / 2) * CM + 8 * ma + r4) * TR + 8 * nb + 2 * c4 + h] =
+              make_double2(t1[ma][nb][h] + t2[ma][nb][h], t3[ma][nb][h] - t1[ma][nb][h] + t2[ma][nb][h]);
+  }
+  __syncthreads();
+  if (w < NW / 2) {
+#pragma unroll
+    for (int ma = 0; ma < MF; ++ma)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double2& slot = red[(w * CM + 8 * ma + r4) * TR + 8 * nb + 2 * c4 + h];
+          slot = make_double2(t1[ma][nb][h] + t2[ma][nb][h] + slot.x,
+                              t3[ma][nb][h] - t1[ma][nb][h] + t2[ma][nb][h] + slot.y);
+        }
+  }
+  __syncthreads();
+  double2* mypart = part + ((size_t)tile * gg.s + split) * (CM * TR);
+  for (int i = threadIdx.x; i < CM * TR; i += NW * 32) {
+    double2 v = red[i];
+#pragma unroll
+    for (int q = 1; q < NW / 2; ++q) v = cadd(v, red[q * CM * TR + i]);
+    mypart[i] = v;
+  }
+  // ---- 2. last CTA of the tile: fixed split-order sum -> C, then release the tile
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&counters[tile], 1u) == (unsigned)gg.s - 1;
+  __syncthreads();
+  const int E = nrows * nocc;
+  if (last) {
+    __threadfence();
+    // G groups of consecutive splits per entry (all their loads in flight),
+    // then the groups in order: fixed summation order for given (s, E)
+    const double2* p0 = part + (size_t)tile * gg.s * (CM * TR);
+    const int G = max(1, min(NW / 2, (NW * 32) / max(E, 1)));
+    const int L = (gg.s + G - 1) / G;
+    for (int j = threadIdx.x; j < G * E; j += NW * 32) {
+      const int q = j / E, e = j - q * E;
+      const int m = e / nrows, i = m * TR + (e - m * nrows);
+      const int s1 = min(gg.s, (q + 1) * L);
+      double2 v = make_double2(0.0, 0.0);
+      for (int sb = q * L; sb < s1; sb += 8) {
+        double2 u[8];
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+          u[qq] = sb + qq < s1 ? __ldcg(&p0[(size_t)(sb + qq) * (CM * TR) + i])
+                               : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) v = cadd(v, u[qq]);
+      }
+      red[q * (CM * TR) + i] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += NW * 32) {
+      const int m = e / nrows, r = e - m * nrows, i = m * TR + r;
+      double2 v = red[i];
+      for (int q = 1; q < G; ++q) v = cadd(v, red[q * (CM * TR) + i]);
+      C[(size_t)(t.row0 + r) * a.ldc + m] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      counters[tile] = 0u;
+      atomicAdd(&flags[tile], 1u);   // publishes C of this tile
+    }
+  } else if (threadIdx.x == 0) {
+    while (*((volatile unsigned*)&flags[tile]) == gen0) __nanosleep(64);
+  }
+  __syncthreads();
+  __threadfence();
+  // ---- 3. Y = X - Phi C on this CTA's chunks, from the smem copies
+  constexpr int CS = CM + 4;   // C tile stride (4 mod 8: conflict-free fragment loads)
+  double2* cs = red;           // reuse: [TR][CS]
+  for (int e = threadIdx.x; e < TR * CS; e += NW * 32) {
+    const int r = e / CS, m = e - r * CS;
+    cs[e] = (r < nrows && m < nocc) ? __ldcg(&C[(size_t)(t.row0 + r) * a.ldc + m])
+                                    : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  int orow[2];
+#pragma unroll
+  for (int jb = 0; jb < 2; ++jb) {
+    const int r = 8 * jb + r4;
+    orow[jb] = r < nrows ? xrow(a, t, r) : -1;
+    if (orow[jb] >= 0 && active && !active[orow[jb] % band_mod]) orow[jb] = -1;
+  }
+  for (int c = 0; c < nc; ++c) {
+    const double2* xs = sm + c * kCoefStage;
+    const double2* ps = xs + TR * RSC;
+    double u1[2][2] = {}, u2[2][2] = {}, u3[2][2] = {};
+    for (int ms = 0; ms < nocc; ms += 4) {
+      const int m = ms + c4;
+      const bool mok = m < nocc;
+      double2 av[2];
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb)   // A[j = r4][k = c4] = C[row j][m]
+        av[jb] = (mok && jb < nfn) ? cs[(8 * jb + r4) * CS + m] : make_double2(0.0, 0.0);
+      const double2 bv = mok ? ps[m * RSC + 8 * w + r4] : make_double2(0.0, 0.0);   // Phi[m][g]
+      const double bsum = bv.x + bv.y;
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb) {
+        if (jb >= nfn) break;
+        dmma(u1[jb][0], u1[jb][1], av[jb].x, bv.x);
+        dmma(u2[jb][0], u2[jb][1], av[jb].y, bv.y);
+        dmma(u3[jb][0], u3[jb][1], av[jb].x + av[jb].y, bsum);
+      }
+    }
+    const size_t g0 = (size_t)(c0 + c) * KC;
+#pragma unroll
+    for (int jb = 0; jb < 2; ++jb) {
+      const int row = orow[jb];
+      if (row < 0) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gl = 8 * w + 2 * c4 + h;
+        const double2 x = xs[(8 * jb + r4) * RSC + gl];
+        const double dr = u1[jb][h] - u2[jb][h];
+        const double di = u3[jb][h] - u1[jb][h] - u2[jb][h];
+        X[(size_t)row * a.nbp + g0 + gl] = make_double2(x.x - dr, x.y - di);
+      }
+    }
+  }
+}
+
+int proj_small(const ProjPlan& pl, ProjArgs a, double2* X, const int* active, int band_mod,
+               double2* part, double2* C, unsigned* flags, cudaStream_t st) {
+  const int cap = plan_tiles(pl);
+  if (cap == 0) return PWB_OK;
+  a.tiles = reinterpret_cast<const ProjTile*>(pl.dtiles.ptr);
+  a.nrows_total = pl.nrows;
+  (void)launch_k(k_proj_small, kSM, NW * 32, kSmallSmem, st, a, X, active,
+                 band_mod > 0 ? band_mod : 1, part, C,
+                 reinterpret_cast<unsigned*>(pl.counters.ptr), flags, (int)pl.tiles.size());
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+bool proj_small_fits(int ntiles, int nbp, int maxocc) {
+  if (maxocc > CM || ntiles <= 0 || ntiles > kSM) return false;
+  const int nchunk = nbp / KC;
+  const int s = (nchunk + kSmallChunks - 1) / kSmallChunks;
+  return (long)s * ntiles <= kSM;
+}
+
+// ---------------------------------------------------------------------------
 static int proj_configure() {
   static bool done = false;
   if (done) return PWB_OK;
   PWB_CUDA(cudaFuncSetAttribute(k_proj_coef, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kCoefSmem));
+  PWB_CUDA(cudaFuncSetAttribute(k_proj_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kSmallSmem));
   PWB_CUDA(cudaFuncSetAttribute(k_proj_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 232448));
   done = true;

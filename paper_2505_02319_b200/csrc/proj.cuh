@@ -78,4 +78,11 @@ int proj_coeffs(const ProjPlan& pl, ProjArgs a, const double2* X, double2* part,
 int proj_apply(const ProjPlan& pl, ProjArgs a, const double2* C, const double2* Xin, double2* Y,
                double ca, double cb, const int* active, int band_mod, cudaStream_t st);
 
+// Fused single-launch Q X for a few tiles of one orbital block (N_occ <= 40):
+// every split's chunks stay in smem from the partial C to the update.
+// flags: one generation counter per tile (persistent, zero-initialised).
+bool proj_small_fits(int ntiles, int nbp, int maxocc);
+int proj_small(const ProjPlan& pl, ProjArgs a, double2* X, const int* active, int band_mod,
+               double2* part, double2* C, unsigned* flags, cudaStream_t st);
+
 }  // namespace pwb

@@ -92,5 +92,6 @@ struct pwb_state {
   pwb::CgBatch cg;           // batch over the shard rows (reused across chi0 calls)
   pwb::CgBatch cg_user;      // batch for pwb_sternheimer calls
   pwb::ProjPlan user_plan;   // pwb_project_out
+  pwb::DevBuf small_flags;   // per-tile generation flags of the fused small projector
   std::vector<int> user_plan_key;
 };
