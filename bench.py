@@ -500,7 +500,7 @@ def run_reference(args):
         vals = []
         t_all = time.perf_counter()
         for _ in range(args.warmup + args.steps):
-            v, sample = oracle_sample(gs, dv0, params, 20.0, threads=ncores)
+            v, sample = oracle_sample(gs, dv0, params, 10.0, threads=ncores)
             vals.append(v)
         value = float(np.mean(vals[args.warmup:]))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
