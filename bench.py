@@ -592,7 +592,10 @@ def main():
     clocks.start()
     launches0 = _lib.launch_count()
     total_ms, n_ham, iters, step_ms = 0.0, 0, [], []
+    region = os.environ.get("PWB_PROFILE_REGION") == "1"   # ncu --profile-from-start off
     barrier()
+    if region:
+        torch.cuda.cudart().cudaProfilerStart()
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -606,6 +609,8 @@ def main():
         n_ham += res.n_ham
         iters.append(res.iterations)
     barrier()
+    if region:
+        torch.cuda.cudart().cudaProfilerStop()
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
     # live per-kernel-group timing (CUDA events on the launching stream) over one more
