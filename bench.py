@@ -80,7 +80,8 @@ def build_workload(cfg):
     if cfg not in (0, 1, 2, 4):
         raise SystemExit(f"config {cfg} is not a Dyson-solve workload")
     spec = synth.build_model(cfg, Lattice, GaussianWell, ModelSpec)
-    gs = run_scf_gpu(spec["model"], kgrid=spec["params"]["kgrid"], tol=1e-9)
+    gs = run_scf_gpu(spec["model"], kgrid=spec["params"]["kgrid"], tol=1e-9,
+                     n_states=spec["params"].get("n_states"))
     g = gs.grids
     dv0 = synth.smoothed_noise(g.g2_cube, g.cube_dims, spec["rng"])
     return gs, dv0, spec["params"]

@@ -60,7 +60,7 @@ CONFIGS = {
             seed=0),
     2: dict(cell=("box", 7.6, 7.6, 76.0), e_cut=20.0, n_electrons=120, n_wells=40,
             temperature=1e-2, smearing="fermi_dirac", xc="lda_x", kgrid=(1, 1, 1), tau=1e-8,
-            strategy="pbal", m=10, seed=0),
+            strategy="pbal", m=10, seed=0, n_states=128),   # 90 states reach the block edge
     3: dict(cell=("cubic", 20.0), e_cut=26.0, n_bands=256, kgrid=(1, 1, 1), seed=0),
     4: dict(cell=("cubic", 20.0), e_cut=12.0, n_electrons=128, n_wells=32, temperature=2e-4,
             smearing="fermi_dirac", xc="lda_x", kgrid=(4, 4, 2), tau=1e-8, strategy="bal", m=10,
