@@ -64,6 +64,8 @@ struct pwb_grid {
   pwb::DevBuf tmp_real;   // scratch real vectors
   pwb::DevBuf red;        // reduction scratch
   pwb::DevBuf scratch;    // small device scalars (GMRES)
+  pwb::DevBuf mgs_part;   // per-CTA partial dots of the fused MGS step
+  pwb::DevBuf mgs_bar;    // its grid-barrier counters
   pwb::DevBuf vt;         // x-major copy of a real multiplier (pencil V product)
 };
 

@@ -81,6 +81,83 @@ __global__ void k_combine(int n, int m, const double* __restrict__ V, const doub
   }
 }
 
+// Grid-wide barrier for a launch whose CTAs are all co-resident (grid <= #SM,
+// 256 threads, no smem): arrival counter + generation (bar zero-initialised
+// once; the last arriver re-arms it).
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vb = bar;
+    const unsigned gen = vb[1];
+    __threadfence();
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(&bar[1], 1u);
+    } else {
+      while (vb[1] == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// sum of this launch's per-CTA partials, fixed order, identical on every CTA
+__device__ __forceinline__ double grid_sum(const double* part, double* red) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += NTV) s += __ldcg(&part[b]);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = NTV / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  const double v = red[0];
+  __syncthreads();
+  return v;
+}
+
+// One Arnoldi step's modified Gram-Schmidt with one re-orthogonalisation
+// (igmres.py:86-103) as ONE launch: per projection, CTA partial dots -> grid
+// barrier -> every CTA sums the partials in the same order and updates its own
+// slice of w (the slice mapping is the same for dot and update, so no other
+// cross-CTA dependency).  2 (i + 1) + 1 barriers instead of 6 (i + 1) + 3
+// launches; hd as in pwb_arnoldi_mgs ([0..i] pass 1, [i+1..2i+1] pass 2, norm).
+__global__ void __launch_bounds__(NTV) k_mgs_fused(int n, int i, const double* __restrict__ V,
+                                                   double* __restrict__ w,
+                                                   double* __restrict__ vnext,
+                                                   double* __restrict__ part,
+                                                   double* __restrict__ hd,
+                                                   unsigned* __restrict__ bar) {
+  pdl_wait();
+  __shared__ double red[NTV];
+  const int nb = gridDim.x;
+  const int i0 = blockIdx.x * NTV + threadIdx.x, st = gridDim.x * NTV;
+  for (int q = 0; q < 2 * (i + 1) + 1; ++q) {
+    const bool norm = q == 2 * (i + 1);
+    const double* vj = norm ? w : V + (size_t)(q % (i + 1)) * n;
+    double acc = 0.0;
+    for (int e = i0; e < n; e += st) acc += vj[e] * w[e];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = NTV / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) part[(size_t)q * nb + blockIdx.x] = red[0];
+    grid_sync(bar);
+    const double h = grid_sum(part + (size_t)q * nb, red);
+    if (!norm) {
+      for (int e = i0; e < n; e += st) w[e] -= h * vj[e];
+      if (blockIdx.x == 0 && threadIdx.x == 0) hd[q] = h;
+    } else {
+      const double d = sqrt(h);
+      for (int e = i0; e < n; e += st) vnext[e] = d > 0.0 ? w[e] / d : 0.0;
+      if (blockIdx.x == 0 && threadIdx.x == 0) hd[q] = d;
+    }
+  }
+}
+
 // vector ops may run without a grid (generic GMRES use): default stream and
 // thread-local scratch
 struct VecCtx {
@@ -130,6 +207,18 @@ int pwb_arnoldi_mgs(pwb_grid* g, int n, int i, double* basis, double* w, double*
   PWB_TRY(c.scratch->ensure((size_t)(2 * (i + 1) + 1) * sizeof(double)));
   double* hd = as<double>(*c.scratch);   // [0..i]: pass 1, [i+1..2i+1]: pass 2, [2i+2]: norm
   const int nb = blocks_for(n);
+  static const bool no_fused = getenv("PWB_NO_FUSED_MGS") != nullptr;   // A/B measurement
+  if (!no_fused && g) {
+    PWB_TRY(g->mgs_part.ensure((size_t)(2 * (i + 1) + 1) * kDotBlocks * sizeof(double)));
+    if (!g->mgs_bar.ptr) {
+      PWB_TRY(g->mgs_bar.ensure(2 * sizeof(unsigned)));
+      PWB_CUDA(cudaMemset(g->mgs_bar.ptr, 0, 2 * sizeof(unsigned)));
+    }
+    (void)launch_k(k_mgs_fused, nb, NTV, 0, c.stream, n, i, (const double*)basis, w,
+                   basis + (size_t)(i + 1) * n, as<double>(g->mgs_part), hd,
+                   as<unsigned>(g->mgs_bar));
+    PWB_LAUNCH_CHECK();
+  } else {
   for (int pass = 0; pass < 2; ++pass)
     for (int j = 0; j <= i; ++j) {
       double* c = hd + pass * (i + 1) + j;
@@ -141,6 +230,7 @@ int pwb_arnoldi_mgs(pwb_grid* g, int n, int i, double* basis, double* w, double*
   PWB_TRY(dot_into(c, n, w, w, nrm, 0, 1));
   (void)launch_k(k_normalise, nb, NTV, 0, c.stream, n, nrm, w, basis + (size_t)(i + 1) * n);
   PWB_LAUNCH_CHECK();
+  }
   std::vector<double> hh(2 * (i + 1) + 1);
   PWB_CUDA(cudaMemcpyAsync(hh.data(), hd, hh.size() * sizeof(double), cudaMemcpyDeviceToHost,
                            c.stream));

@@ -202,27 +202,34 @@ class DeviceState:
         With sharding active the result is already all-reduced over ranks, and
         the returned iteration counts cover the whole (k, n) list (all-gathered).
         """
+        self.chi0_begin(dv_t)
+        return self.chi0_finish(tol)
+
+    def chi0_begin(self, dv_t):
+        """Launch the right-hand side of chi0 dv (asynchronous: the host is free to
+        compute the tolerance vector while the GPU builds the RHS)."""
+        b0, b1 = self.shard
+        self._dv_pending = dv_t   # keep the input alive until finish
+        _lib.check(self._lib.pwb_chi0_begin(self.handle, b0, b1, ptr(dv_t), ptr(self._fsum)),
+                   "chi0_begin")
+        if self.comm is not None and abs(self.fp_den) > self.fp_thresh:
+            import torch.distributed as dist
+            dist.all_reduce(self._fsum[:1], group=self.comm[2])   # global delta eps_F (metals)
+
+    def chi0_finish(self, tol):
+        """Sternheimer solves + delta rho accumulation of the pending chi0."""
         torch = torch_mod()
         tol = np.ascontiguousarray(tol, dtype=float)
         drho = torch.empty(self.grid.n_g, dtype=torch.float64, device=self.device)
         b0, b1 = self.shard
-        if self.comm is None and (b0, b1) == (0, self.nband):
-            its = np.zeros(self.nband, dtype=np.int32)
-            status = self._lib.pwb_chi0(self.handle, ptr(dv_t), _np_ptr(tol), ptr(drho),
-                                        _np_ptr(its))
-            _lib.check(status, "chi0")
-            return drho, its
-        import torch.distributed as dist
-        rank, world, group = self.comm if self.comm else (0, 1, None)
-        _lib.check(self._lib.pwb_chi0_begin(self.handle, b0, b1, ptr(dv_t), ptr(self._fsum)),
-                   "chi0_begin")
-        if self.comm is not None and abs(self.fp_den) > self.fp_thresh:
-            dist.all_reduce(self._fsum[:1], group=group)   # global delta eps_F (metals)
         its_local = np.zeros(max(b1 - b0, 1), dtype=np.int32)
         tl = np.ascontiguousarray(tol[b0:b1]) if b1 > b0 else np.zeros(1)
         status = self._lib.pwb_chi0_finish(self.handle, ptr(self._fsum), _np_ptr(tl), ptr(drho),
                                            _np_ptr(its_local))
+        self._dv_pending = None
         if self.comm is not None:
+            import torch.distributed as dist
+            group = self.comm[2]
             dist.all_reduce(drho, group=group)
             cnt = torch.zeros(self.nband, dtype=torch.int64, device=self.device)
             cnt[b0:b1] = torch.from_numpy(its_local[: b1 - b0].astype(np.int64)).to(self.device)

@@ -72,16 +72,21 @@ def _to_dev(ds, v):
     return torch.from_numpy(v).to(ds.device)
 
 
+def _stats(its, tols):
+    """Chi0Stats of one apply; adds the H applications to ham_counter (groundstate.py:48)."""
+    its = [int(i) for i in its]
+    total = int(sum(its))
+    ham_counter.add(total)
+    return Chi0Stats(cg_iterations_per_band=its, tolerances_used=list(tols),
+                     ham_applications=total)
+
+
 def apply_chi0_dev(gs, dv_t, tolerances):
     """Device-resident chi0: (drho tensor, Chi0Stats); dv_t a float64 device tensor."""
     tols = _validate(gs, tolerances)
     ds = device_state(gs)
     drho, its = ds.chi0(_to_dev(ds, dv_t), tols)
-    its = [int(i) for i in its]
-    total = int(sum(its))
-    ham_counter.add(total)
-    return drho, Chi0Stats(cg_iterations_per_band=its, tolerances_used=list(tols),
-                           ham_applications=total)
+    return drho, _stats(its, tols)
 
 
 def apply_chi0(gs, dv, tolerances, threads=1):
@@ -147,8 +152,15 @@ def apply_dielectric_dev(gs, kernel, v_t, tolerances):
     kv = _norm(ds.grid, u)
     if kv == 0.0:
         return v_t.clone(), 0.0, None
-    tol_vec = tolerances(kv) if callable(tolerances) else tolerances
-    drho, stats = apply_chi0_dev(gs, u / kv, tol_vec)
+    if callable(tolerances):
+        # the tolerance vector depends on |Kv| only: build chi0's right-hand side on
+        # the GPU while the host evaluates the strategy (strategies.py, numpy)
+        ds.chi0_begin(u / kv)
+        tols = _validate(gs, tolerances(kv))
+        drho, its = ds.chi0_finish(tols)
+        stats = _stats(its, tols)
+    else:
+        drho, stats = apply_chi0_dev(gs, u / kv, tolerances)
     return v_t - kv * drho, kv, stats
 
 
