@@ -283,6 +283,8 @@ __global__ void k_loop_ctl(cudaGraphConditionalHandle h, int* __restrict__ hdr) 
 }
 
 CgBatch::~CgBatch() {
+  if (h_its) cudaFreeHost(h_its);
+  if (h_res) cudaFreeHost(h_res);
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
   if (graph_stream) cudaStreamDestroy(graph_stream);
@@ -548,7 +550,7 @@ static int ensure_graph(pwb_state* st, CgBatch& cg) {
 
 // Run the batched PCG on cg.rhs with tolerances tol (host); x = rows [0, n) of cg.xr.
 int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max_iter,
-             int* iters_host, double* res_host) {
+             int* iters_host, double* res_host, bool defer) {
   pwb_grid* g = st->g;
   cudaStream_t s = g->stream;
   const int n = cg.nrows;
@@ -585,12 +587,22 @@ int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max
     cg.graph_w = g->wbuf.ptr;
   }
   cg.prof_rows = n;   // rows active in the next iteration (profiling units only)
-  if (use_graph && cg.loop_graph) {   // the whole loop on the device
+  if (cg.h_rows < n) {
+    if (cg.h_its) cudaFreeHost(cg.h_its);
+    if (cg.h_res) cudaFreeHost(cg.h_res);
+    PWB_CUDA(cudaMallocHost(&cg.h_its, (size_t)n * sizeof(int)));
+    PWB_CUDA(cudaMallocHost(&cg.h_res, (size_t)n * sizeof(double)));
+    cg.h_rows = n;
+  }
+  cg.loop_ran = use_graph && cg.loop_graph;
+  if (cg.loop_ran) {   // the whole loop on the device; results read back with the header
     PWB_CUDA(cudaGraphLaunch(cg.exec, s));
     PWB_CUDA(cudaMemcpyAsync(cg.h_hdr, cg.ctl.hdr, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    PWB_CUDA(cudaMemcpyAsync(cg.h_its, cg.s.iters, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+    PWB_CUDA(cudaMemcpyAsync(cg.h_res, cg.s.res, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (defer) return PWB_OK;
     PWB_CUDA(cudaStreamSynchronize(s));
-    count_launch((int)(g_iter_launches * (unsigned long long)std::max(cg.h_hdr[5], 1)));
-    if (cg.h_hdr[3] != 0) return fail(PWB_ERR_NONCONV, "Sternheimer CG: iteration cap reached");
+    return cg_check(cg, tol, iters_host, res_host);
   }
   for (; !(use_graph && cg.loop_graph);) {
     if (use_graph) {
@@ -606,12 +618,24 @@ int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max
     if (cg.h_hdr[3] == 0) break;   // no row still iterating
   }
   prof().rows_hint = 0;
-  const bool failed = cg.h_hdr[4] != 0;
-  std::vector<int> its(n);
-  std::vector<double> res(n);
-  PWB_CUDA(cudaMemcpyAsync(its.data(), cg.s.iters, n * sizeof(int), cudaMemcpyDeviceToHost, s));
-  PWB_CUDA(cudaMemcpyAsync(res.data(), cg.s.res, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  PWB_CUDA(cudaMemcpyAsync(cg.h_its, cg.s.iters, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+  PWB_CUDA(cudaMemcpyAsync(cg.h_res, cg.s.res, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (defer) return PWB_OK;
   PWB_CUDA(cudaStreamSynchronize(s));
+  return cg_check(cg, tol, iters_host, res_host);
+}
+
+// Verdict of a finished batch from the read-back header and per-row results
+// (the stream has been synchronised): reference sternheimer.py:83-90 errors.
+int cg_check(CgBatch& cg, const std::vector<double>& tol, int* iters_host, double* res_host) {
+  const int n = cg.nrows;
+  if (cg.loop_ran) {
+    count_launch((int)(g_iter_launches * (unsigned long long)std::max(cg.h_hdr[5], 1)));
+    if (cg.h_hdr[3] != 0) return fail(PWB_ERR_NONCONV, "Sternheimer CG: iteration cap reached");
+  }
+  const bool failed = cg.h_hdr[4] != 0;
+  int* its = cg.h_its;
+  const double* res = cg.h_res;
   int first_fail = -1;
   for (int i = 0; i < n; ++i) {
     if (res[i] > tol[i]) {

@@ -319,7 +319,8 @@ int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, d
   PWB_TRY(proj_apply(cg.plan1, a, as<double2>(st->cm), as<double2>(st->dvpsi),
                      as<double2>(cg.rhs), -1.0, 1.0, nullptr, n, s));
   std::vector<double> tol(tol_host, tol_host + n);
-  PWB_TRY(cg_solve(st, cg, tol, -1, iters_host, nullptr));
+  // results are read back with the accumulation already queued behind the CG loop
+  PWB_TRY(cg_solve(st, cg, tol, -1, nullptr, nullptr, true));
   // drho accumulation (response.py:150-154)
   double2* W = as<double2>(g->wbuf);
   const int* bk = as<int>(st->d_band_k) + b0;
@@ -334,7 +335,7 @@ int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, d
   prof().end(PROF_ACC, ea, s, n);
   PWB_CUDA(cudaStreamSynchronize(s));
   prof().flush();
-  return PWB_OK;
+  return cg_check(cg, tol, iters_host, nullptr);
 }
 
 int pwb_chi0(pwb_state* st, const double* dv, const double* tol_host, double* drho,

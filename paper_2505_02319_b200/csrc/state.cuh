@@ -44,6 +44,10 @@ struct CgBatch {
   IterCtl ctl;
   CgScalars s;
   int* h_hdr = nullptr;     // pinned copy of ctl.hdr
+  int* h_its = nullptr;     // pinned per-row iteration counts / residuals (readback)
+  double* h_res = nullptr;
+  int h_rows = 0;
+  bool loop_ran = false;    // the last cg_solve ran the device-loop graph
   int max_tiles = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -62,8 +66,11 @@ int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* activ
                  const int* rows, double2* part, double2* cmat, cudaStream_t s,
                  const int* ntiles = nullptr, int mult = 1);
 int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands);
+// defer: enqueue the result readback and return without synchronising; the
+// caller synchronises the stream (after queueing more work) and calls cg_check
 int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max_iter,
-             int* iters_host, double* res_host);
+             int* iters_host, double* res_host, bool defer = false);
+int cg_check(CgBatch& cg, const std::vector<double>& tol, int* iters_host, double* res_host);
 
 // accumulation kernels (chi0.cu)
 int launch_drho_partial(pwb_grid* g, int nband, const double2* W, const double2* psir,
