@@ -25,7 +25,10 @@
 
 namespace pwb {
 
-constexpr int NTC = 256;
+#ifndef PWB_NTC
+#define PWB_NTC 1024   // 1024: 11% lower 1-row iteration latency, 2.5% at 261 rows (tools/iter_latency.py)
+#endif
+constexpr int NTC = PWB_NTC;   // threads per row of the CG vector kernels
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
