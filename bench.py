@@ -18,6 +18,7 @@ reference, oracle/) on the host cores with the same config and metric.
 """
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -429,10 +430,13 @@ def run_microbench(args):
     clocks.start()
     launches0 = _lib.launch_count()
     step_ms = []
+    gc.collect()
+    gc.disable()   # no cyclic-GC pause inside the timed steps
     for _ in range(args.steps):
         flush.zero_()
         step_ms.append(timed(step, 1))
     launches = _lib.launch_count() - launches0
+    gc.enable()
     clk = clocks.stop()
     ms_step = float(np.mean(step_ms))
     # the two kernel groups alone (inputs larger than L2: 256 rows x 50 685 x 16 B = 207 MB)
@@ -594,6 +598,10 @@ def main():
     launches0 = _lib.launch_count()
     total_ms, n_ham, iters, step_ms = 0.0, 0, [], []
     region = os.environ.get("PWB_PROFILE_REGION") == "1"   # ncu --profile-from-start off
+    # a full cyclic-GC pass of this process (torch + scipy heaps) stalls the host
+    # launch stream for ~0.1 s at random points: collect now, none while timing
+    gc.collect()
+    gc.disable()
     barrier()
     if region:
         torch.cuda.cudart().cudaProfilerStart()
@@ -613,6 +621,7 @@ def main():
     if region:
         torch.cuda.cudart().cudaProfilerStop()
     launches = _lib.launch_count() - launches0
+    gc.enable()
     clk = clocks.stop()
     # live per-kernel-group timing (CUDA events on the launching stream) over one more
     # identical solve; kept out of the timed loop so event records do not perturb it
@@ -633,6 +642,8 @@ def main():
     pinned = torch.from_numpy(dv0).pin_memory()
     e2e_ms, e2e_ham, e2e_list = 0.0, 0, []
     e2e_steps = max(1, min(args.steps, 3))
+    gc.collect()
+    gc.disable()
     barrier()
     for _ in range(e2e_steps):
         flush.zero_()
@@ -648,6 +659,7 @@ def main():
         e2e_ms += e2e_list[-1]
         e2e_ham += r.n_ham
         del sol
+    gc.enable()
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
