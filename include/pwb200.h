@@ -146,6 +146,40 @@ int pwb_chi0_begin(pwb_state* st, int b0, int b1, const double* dv, double* fsum
 int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, double* drho,
                     int* iters_host);
 
+/* ---- sharded chi0 with ONE all-reduce per apply --
+ * The reference's only parallelism is the band thread pool of apply_chi0
+ * (response.py:144-148); these entry points split the (k, n) list over ranks
+ * instead.  After pwb_chi0_begin(b0, b1) a rank calls pwb_chi0_finish_local,
+ * which runs its Sternheimer solves and accumulation with delta eps_F = 0 and
+ * writes a packet of pwb_chi0_packet_size doubles (device):
+ *   [drho partial (n_g) | C(r) = sum w f' |psi|^2 (n_g, metals only) |
+ *    sum w f' delta eps | failed rows | CG iterations per global row (nband) |
+ *    residual of each failed row, else 0 (nband)].
+ * The packets are summed over ranks (pwb_allreduce: ncclAllReduce on the
+ * state's stream through the communicator of pwb_comm_init, or any other
+ * sum); pwb_chi0_reduce_apply then forms drho = sum - delta eps_F C(r) with
+ * the global delta eps_F (response.py:131-136, summed over k) and returns the
+ * iteration counts of ALL rows, failing with PWB_ERR_NONCONV on every rank if
+ * any rank's row failed (residual_host = the first failed row's residual).
+ * pwb_chi0_finish_sharded = local + pwb_allreduce + reduce_apply.            */
+int pwb_chi0_packet_size(pwb_state* st, long long* n);
+int pwb_chi0_finish_local(pwb_state* st, const double* fsum, const double* tol_host,
+                          double* packet);
+int pwb_chi0_reduce_apply(pwb_state* st, const double* packet, double* drho, int* iters_host,
+                          double* residual_host);
+int pwb_chi0_finish_sharded(pwb_state* st, const double* fsum, const double* tol_host,
+                            double* packet, double* drho, int* iters_host, double* residual_host);
+/* NCCL communicator of a state (NCCL resolved at run time, libnccl.so.2):
+ * rank 0 calls pwb_comm_unique_id (128-byte ncclUniqueId), the caller
+ * broadcasts it, every rank calls pwb_comm_init with it.                     */
+int pwb_comm_unique_id(void* id_out);
+int pwb_comm_init(pwb_state* st, const void* id, int rank, int nranks);
+int pwb_comm_destroy(pwb_state* st);
+/* in-place sum all-reduce of n device doubles on the state's stream          */
+int pwb_allreduce(pwb_state* st, double* buf, long long n);
+/* residual carried by the last PWB_ERR_NONCONV of this thread (NaN if none)  */
+double pwb_last_residual(void);
+
 /* orbital_row_norm (response.py:190-199): max_r sqrt(sum_n |psi_n(r)|^2)
  * (real part only when real_part != 0) over k block k.                       */
 int pwb_row_norm(pwb_state* st, int k, int real_part, double* out_host);

@@ -67,6 +67,15 @@ SIGNATURES = {
     "pwb_vec_axpy": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_double, _vp, _vp]),
     "pwb_arnoldi_mgs": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
     "pwb_vec_combine": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "pwb_chi0_packet_size": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_longlong)]),
+    "pwb_chi0_finish_local": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "pwb_chi0_reduce_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp, _c_dbl_p]),
+    "pwb_chi0_finish_sharded": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_dbl_p]),
+    "pwb_comm_unique_id": (ctypes.c_int, [_vp]),
+    "pwb_comm_init": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int]),
+    "pwb_comm_destroy": (ctypes.c_int, [_vp]),
+    "pwb_allreduce": (ctypes.c_int, [_vp, _vp, ctypes.c_longlong]),
+    "pwb_last_residual": (ctypes.c_double, []),
 }
 
 _lock = threading.Lock()
@@ -108,7 +117,8 @@ def check(status, what=""):
     if status == PWB_ERR_CONFIG:
         raise ConfigurationError(msg)
     if status == PWB_ERR_NONCONV:
-        raise NonConvergenceError(msg)
+        res = float(load().pwb_last_residual())
+        raise NonConvergenceError(msg, residual=None if res != res else res)
     if status in (PWB_ERR_CUDA, PWB_ERR_NOMEM):
         raise DeviceError(msg)
     raise PwdysonError(msg)

@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpwb200.so")
-SOURCES = ["grid.cu", "fft_kernels.cu", "proj.cu", "state.cu", "cg.cu", "chi0.cu", "vec.cu"]
+SOURCES = ["grid.cu", "fft_kernels.cu", "proj.cu", "state.cu", "cg.cu", "chi0.cu", "vec.cu", "comm.cu"]
 HEADERS = ["common.cuh", "fft_engine.cuh", "grid.cuh", "proj.cuh", "state.cuh", "profile.cuh", "fft_static.cuh", "dispatch.cuh", "tma.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
@@ -63,7 +63,7 @@ def build(force=False, verbose=False, variant="", defines=()):
             print(out.decode())
     tmp = lib + ".tmp"
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
-           "-lcudart"]
+           "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")

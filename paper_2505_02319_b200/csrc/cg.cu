@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(NTC) k_cg_init2(GridDev g, CgScalars sc, int n
   __shared__ double red[NTC / 32 + 1];
   const int row = blockIdx.x;
   if (row == 0 && threadIdx.x == 0) {   // device-side iteration loop: counter and cap
+    hdr[4] = 0;   // max_iter failure flag: sticky over the whole solve
     hdr[5] = 0;
     hdr[6] = cap;
   }
@@ -260,7 +261,6 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
     ctl.hdr[1] = t;
     ctl.hdr[2] = 2 * t;
     ctl.hdr[3] = 0;   // rows still iterating after this iteration (k_cg_resid counts)
-    ctl.hdr[4] = 0;   // max_iter failure flag
     carry = t;
   }
   __syncthreads();
@@ -578,7 +578,8 @@ int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max
   if (g->wbuf.bytes < wbytes || !g->wbuf.ptr) {
     PWB_TRY(g->wbuf.ensure(wbytes));
   }
-  if (cg.exec && cg.graph_w != g->wbuf.ptr) {   // a captured pointer moved
+  if (cg.exec && (cg.graph_w != g->wbuf.ptr || cg.graph_part != cg.part.ptr ||
+                  cg.graph_cmat != cg.cmat.ptr)) {   // a captured pointer moved
     cudaGraphExecDestroy(cg.exec);
     cudaGraphDestroy(cg.graph);
     cg.exec = nullptr;
@@ -588,6 +589,8 @@ int cg_solve(pwb_state* st, CgBatch& cg, const std::vector<double>& tol, int max
   if (use_graph) {
     PWB_TRY(ensure_graph(st, cg));
     cg.graph_w = g->wbuf.ptr;
+    cg.graph_part = cg.part.ptr;
+    cg.graph_cmat = cg.cmat.ptr;
   }
   cg.prof_rows = n;   // rows active in the next iteration (profiling units only)
   if (cg.h_rows < n) {
@@ -641,7 +644,7 @@ int cg_check(CgBatch& cg, const std::vector<double>& tol, int* iters_host, doubl
   const double* res = cg.h_res;
   int first_fail = -1;
   for (int i = 0; i < n; ++i) {
-    if (res[i] > tol[i]) {
+    if (!(res[i] <= tol[i])) {   // NaN residuals fail too
       if (first_fail < 0) first_fail = i;
       its[i] = -1;
     }
@@ -649,6 +652,7 @@ int cg_check(CgBatch& cg, const std::vector<double>& tol, int* iters_host, doubl
     if (res_host) res_host[i] = res[i];
   }
   if (failed || first_fail >= 0) {
+    set_last_residual(first_fail >= 0 ? res[first_fail] : NAN);
     char buf[256];
     snprintf(buf, sizeof(buf), "Sternheimer CG for band %d stalled at %.3e (target %.3e)",
              first_fail >= 0 ? cg.bands[first_fail] : -1,

@@ -70,6 +70,61 @@ __global__ void k_chi0_occ(int r0, int nrows, int ldc, const int* __restrict__ b
   }
 }
 
+// C(r) = sum_b w_b f'_b |psi_b(r)|^2 over the shard rows (x-fastest output):
+// the delta eps_F coefficient of drho, folded in after the sharded all-reduce
+__global__ void k_fermi_density(int nx, int nyz, int nband, const double2* __restrict__ psir,
+                                const double* __restrict__ coef, int b0, double* __restrict__ out) {
+  pdl_wait();
+  const long long ng = (long long)nx * nyz;
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // x-major index
+  if (j >= ng) return;
+  double s = 0.0;
+  for (int b = 0; b < nband; ++b) {
+    const double2 p = psir[(size_t)b * ng + j];
+    s += coef[4 * (b0 + b) + 1] * (p.x * p.x + p.y * p.y);
+  }
+  const int x = (int)(j / nyz), t = (int)(j - (long long)x * nyz);
+  out[(size_t)t * nx + x] = s;
+}
+
+// packet tail of one rank: [0] sum w f' delta eps (metals), [1] failed rows,
+// [2 + b] CG iterations of global row b, [2 + nband + b] residual if row b failed
+__global__ void k_pack_tail(int n, int b0, int nband, const int* __restrict__ iters,
+                            const double* __restrict__ res, const double* __restrict__ tol,
+                            const int* __restrict__ hdr, const double* __restrict__ fsum,
+                            int metal, double* __restrict__ tail) {
+  pdl_wait();
+  __shared__ int nfail;
+  if (threadIdx.x == 0) nfail = 0;
+  __syncthreads();
+  int f = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    tail[2 + b0 + i] = (double)iters[i];
+    const double r = res[i];
+    if (!(r <= tol[i])) {
+      tail[2 + nband + b0 + i] = (r == 0.0) ? 1e-300 : r;
+      ++f;
+    }
+  }
+  if (f) atomicAdd(&nfail, f);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tail[0] = metal ? fsum[0] : 0.0;
+    tail[1] = (double)(nfail + (hdr[3] > 0 ? 1 : 0));   // hdr[3] > 0: loop cap reached
+  }
+}
+
+// drho = sum of partials - delta eps_F C(r), delta eps_F = sum w f' delta eps / sum w f'
+__global__ void k_fermi_apply(long long ng, const double* __restrict__ packet, int metal, double den,
+                              double* __restrict__ drho) {
+  pdl_wait();
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ng) return;
+  double v = packet[i];
+  if (metal) v -= (packet[2 * ng] / den) * packet[ng + i];
+  drho[i] = v;
+}
+
 // psi(r) cache for rows [b0, b1)
 static int ensure_psir(pwb_state* st, int b0, int b1) {
   if (st->psir_b0 == b0 && st->psir_b1 == b1) return PWB_OK;
@@ -219,11 +274,10 @@ int pwb_project_out(pwb_state* st, int k, int ncol, double* x) {
     PWB_TRY(proj_plan(st->user_plan, key, st->nocc, st->g->nbp));
     st->user_plan_key = key;
   }
-  CgBatch& cg = st->cg_user;
-  PWB_TRY(cg.part.ensure(proj_part_elems(st->user_plan) * sizeof(double2)));
-  PWB_TRY(cg.cmat.ensure((size_t)ncol * st->ldc * sizeof(double2)));
+  PWB_TRY(st->user_part.ensure(proj_part_elems(st->user_plan) * sizeof(double2)));
+  PWB_TRY(st->user_cmat.ensure((size_t)ncol * st->ldc * sizeof(double2)));
   return project_rows(st, st->user_plan, reinterpret_cast<double2*>(x), nullptr, ncol, nullptr,
-                      as<double2>(cg.part), as<double2>(cg.cmat), st->g->stream);
+                      as<double2>(st->user_part), as<double2>(st->user_cmat), st->g->stream);
 }
 
 int pwb_sternheimer(pwb_state* st, int nrhs, const int* band_host, const double* rhs,
@@ -291,24 +345,24 @@ int pwb_chi0_begin(pwb_state* st, int b0, int b1, const double* dv, double* fsum
   return PWB_OK;
 }
 
-int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, double* drho,
-                    int* iters_host) {
-  if (!st) return fail(PWB_ERR_VALUE, "null state");
+// Sternheimer solves + accumulation of the pending chi0 into drho.  den /
+// thresh decide the Fermi-level shift (response.py:131-136): the state's
+// sum_k w_k sum_n f'_n for the full formula, or (0, 1) for delta eps_F = 0
+// (the sharded form folds the shift in after the all-reduce).  check = false
+// leaves the CG verdict on the device (k_pack_tail reads it) and does not
+// synchronise.
+static int chi0_finish_impl(pwb_state* st, const double* fsum, double den, double thresh,
+                            const double* tol_host, double* drho, int* iters_host, bool check) {
   pwb_grid* g = st->g;
   cudaStream_t s = g->stream;
   const int b0 = st->shard_b0, b1 = st->shard_b1, n = b1 - b0;
-  if (n == 0) {
-    PWB_CUDA(cudaMemsetAsync(drho, 0, (size_t)g->ng * sizeof(double), s));
-    PWB_CUDA(cudaStreamSynchronize(s));
-    return PWB_OK;
-  }
   CgBatch& cg = st->cg;
   double* deps = as<double>(st->scal);
   double* c2 = deps + n;
   double* c1 = deps + 2 * n;
   ProjArgs a = proj_args(st);
   (void)launch_k(k_chi0_occ, n, 64, 0, s, b0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_nocc),
-                              as<double>(st->d_coef), fsum, st->fp_den, st->fp_thresh, deps,
+                              as<double>(st->d_coef), fsum, den, thresh, deps,
                               as<double>(st->wt), as<double2>(st->cm), as<double2>(st->cw), c2,
                               c1);
   PWB_LAUNCH_CHECK();
@@ -333,9 +387,121 @@ int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, d
                               as<double>(st->drho_part)));
   PWB_TRY(launch_drho_reduce(g, nchunk, as<double>(st->drho_part), drho));
   prof().end(PROF_ACC, ea, s, n);
+  if (!check) return PWB_OK;
   PWB_CUDA(cudaStreamSynchronize(s));
   prof().flush();
   return cg_check(cg, tol, iters_host, nullptr);
+}
+
+int pwb_chi0_finish(pwb_state* st, const double* fsum, const double* tol_host, double* drho,
+                    int* iters_host) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  pwb_grid* g = st->g;
+  cudaStream_t s = g->stream;
+  if (st->shard_b1 == st->shard_b0) {
+    PWB_CUDA(cudaMemsetAsync(drho, 0, (size_t)g->ng * sizeof(double), s));
+    PWB_CUDA(cudaStreamSynchronize(s));
+    return PWB_OK;
+  }
+  return chi0_finish_impl(st, fsum, st->fp_den, st->fp_thresh, tol_host, drho, iters_host, true);
+}
+
+// ---- sharded chi0: one all-reduce per apply ----------------------------------------
+static bool is_metal(const pwb_state* st) { return std::fabs(st->fp_den) > st->fp_thresh; }
+
+int pwb_chi0_packet_size(pwb_state* st, long long* n) {
+  if (!st || !n) return fail(PWB_ERR_VALUE, "null argument");
+  const long long ng = st->g->ng;
+  *n = ng * (is_metal(st) ? 2 : 1) + 2 + 2LL * st->nband;
+  return PWB_OK;
+}
+
+int pwb_chi0_finish_local(pwb_state* st, const double* fsum, const double* tol_host,
+                          double* packet) {
+  if (!st || !packet) return fail(PWB_ERR_VALUE, "null argument");
+  pwb_grid* g = st->g;
+  cudaStream_t s = g->stream;
+  const int b0 = st->shard_b0, n = st->shard_b1 - b0;
+  const size_t ng = g->ng;
+  const bool metal = is_metal(st);
+  double* tail = packet + ng * (metal ? 2 : 1);
+  PWB_CUDA(cudaMemsetAsync(tail, 0, (2 + 2 * (size_t)st->nband) * sizeof(double), s));
+  if (n == 0) {
+    PWB_CUDA(cudaMemsetAsync(packet, 0, ng * (metal ? 2 : 1) * sizeof(double), s));
+    return PWB_OK;
+  }
+  // delta eps_F = 0 here: the shift is global over all ranks' bands
+  PWB_TRY(chi0_finish_impl(st, fsum, 0.0, 1.0, tol_host, packet, nullptr, false));
+  if (metal) {
+    if (st->fermi_b0 != st->shard_b0 || st->fermi_b1 != st->shard_b1) {
+      PWB_TRY(st->fermi_c.ensure(ng * sizeof(double)));
+      (void)launch_k(k_fermi_density, (unsigned)((ng + 255) / 256), 256, 0, s, g->nx, g->nyz, n,
+                     as<double2>(st->psir), as<double>(st->d_coef), b0, as<double>(st->fermi_c));
+      PWB_LAUNCH_CHECK();
+      st->fermi_b0 = st->shard_b0;
+      st->fermi_b1 = st->shard_b1;
+    }
+    PWB_CUDA(cudaMemcpyAsync(packet + ng, st->fermi_c.ptr, ng * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
+  }
+  CgBatch& cg = st->cg;
+  (void)launch_k(k_pack_tail, 1, 256, 0, s, n, b0, st->nband, cg.s.iters, cg.s.res, cg.s.tol,
+                 cg.ctl.hdr, fsum, metal ? 1 : 0, tail);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int pwb_chi0_reduce_apply(pwb_state* st, const double* packet, double* drho, int* iters_host,
+                          double* residual_host) {
+  if (!st || !packet || !drho) return fail(PWB_ERR_VALUE, "null argument");
+  pwb_grid* g = st->g;
+  cudaStream_t s = g->stream;
+  const size_t ng = g->ng;
+  const bool metal = is_metal(st);
+  const double* tail = packet + ng * (metal ? 2 : 1);
+  (void)launch_k(k_fermi_apply, (unsigned)((ng + 255) / 256), 256, 0, s, (long long)ng, packet,
+                 metal ? 1 : 0, st->fp_den, drho);
+  PWB_LAUNCH_CHECK();
+  const size_t nt = 2 + 2 * (size_t)st->nband;
+  if (st->h_tail_n < nt) {
+    if (st->h_tail) cudaFreeHost(st->h_tail);
+    st->h_tail = nullptr;
+    PWB_CUDA(cudaMallocHost(&st->h_tail, nt * sizeof(double)));
+    st->h_tail_n = nt;
+  }
+  PWB_CUDA(cudaMemcpyAsync(st->h_tail, tail, nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+  PWB_CUDA(cudaStreamSynchronize(s));
+  prof().flush();
+  const double* t = st->h_tail;
+  const int nb = st->nband;
+  int first_fail = -1;
+  for (int b = 0; b < nb; ++b) {
+    const double r = t[2 + nb + b];
+    const bool bad = r != 0.0;   // residual of a failed row (NaN included), 0 otherwise
+    if (bad && first_fail < 0) first_fail = b;
+    if (iters_host) iters_host[b] = bad ? -1 : (int)t[2 + b];
+  }
+  if (t[1] > 0.0) {
+    const double r = first_fail >= 0 ? t[2 + nb + first_fail] : NAN;
+    if (residual_host) *residual_host = r;
+    set_last_residual(r);
+    char buf[256];
+    snprintf(buf, sizeof(buf), "Sternheimer CG for band %d stalled at %.3e (%g rows failed "
+             "over all ranks)", first_fail, r, t[1]);
+    return fail(PWB_ERR_NONCONV, buf);
+  }
+  return PWB_OK;
+}
+
+int pwb_chi0_finish_sharded(pwb_state* st, const double* fsum, const double* tol_host,
+                            double* packet, double* drho, int* iters_host, double* residual_host) {
+  if (!st) return fail(PWB_ERR_VALUE, "null state");
+  if (!st->comm) return fail(PWB_ERR_CONFIG, "no communicator: call pwb_comm_init first");
+  long long n = 0;
+  PWB_TRY(pwb_chi0_packet_size(st, &n));
+  PWB_TRY(pwb_chi0_finish_local(st, fsum, tol_host, packet));
+  PWB_TRY(pwb_allreduce(st, packet, n));
+  return pwb_chi0_reduce_apply(st, packet, drho, iters_host, residual_host);
 }
 
 int pwb_chi0(pwb_state* st, const double* dv, const double* tol_host, double* drho,

@@ -53,6 +53,8 @@ struct CgBatch {
   cudaGraphExec_t exec = nullptr;
   cudaStream_t graph_stream = nullptr;
   void* graph_w = nullptr;  // plane buffer captured in the graph
+  void* graph_part = nullptr;   // GEMM scratch captured in the graph
+  void* graph_cmat = nullptr;
   bool loop_graph = false;  // graph = WHILE conditional node around one iteration
   int prof_rows = 0;        // active rows of the running iteration (profiler units)
   ~CgBatch();
@@ -99,6 +101,22 @@ struct pwb_state {
   pwb::CgBatch cg;           // batch over the shard rows (reused across chi0 calls)
   pwb::CgBatch cg_user;      // batch for pwb_sternheimer calls
   pwb::ProjPlan user_plan;   // pwb_project_out
+  pwb::DevBuf user_part, user_cmat;   // pwb_project_out scratch (never cg_user's: its graph
+                                      // captured cg_user.part / cmat pointers)
   pwb::DevBuf small_flags;   // per-tile generation flags of the fused small projector
   std::vector<int> user_plan_key;
+  // sharded chi0 (comm.cu): NCCL communicator, cached C(r) of the shard rows,
+  // pinned readback of the reduced packet tail
+  void* comm = nullptr;
+  pwb::DevBuf fermi_c;
+  int fermi_b0 = -1, fermi_b1 = -1;
+  double* h_tail = nullptr;
+  size_t h_tail_n = 0;
+  ~pwb_state();
 };
+
+extern "C" int pwb_allreduce(pwb_state* st, double* buf, long long n);
+namespace pwb {
+void set_last_residual(double r);
+int comm_destroy(pwb_state* st);
+}

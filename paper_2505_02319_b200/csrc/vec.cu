@@ -208,17 +208,27 @@ int pwb_arnoldi_mgs(pwb_grid* g, int n, int i, double* basis, double* w, double*
   double* hd = as<double>(*c.scratch);   // [0..i]: pass 1, [i+1..2i+1]: pass 2, [2i+2]: norm
   const int nb = blocks_for(n);
   static const bool no_fused = getenv("PWB_NO_FUSED_MGS") != nullptr;   // A/B measurement
-  if (!no_fused && g) {
+  bool fused = !no_fused && g;
+  if (fused) {
     PWB_TRY(g->mgs_part.ensure((size_t)(2 * (i + 1) + 1) * kDotBlocks * sizeof(double)));
     if (!g->mgs_bar.ptr) {
       PWB_TRY(g->mgs_bar.ensure(2 * sizeof(unsigned)));
       PWB_CUDA(cudaMemset(g->mgs_bar.ptr, 0, 2 * sizeof(unsigned)));
     }
-    (void)launch_k(k_mgs_fused, nb, NTV, 0, c.stream, n, i, (const double*)basis, w,
-                   basis + (size_t)(i + 1) * n, as<double>(g->mgs_part), hd,
-                   as<unsigned>(g->mgs_bar));
-    PWB_LAUNCH_CHECK();
-  } else {
+    // the grid barrier needs every CTA resident: cooperative launch, which fails
+    // (instead of hanging) when SM partitioning / concurrent kernels prevent it;
+    // then the unfused dot / axpy sequence below runs instead
+    const cudaError_t e = launch_coop(k_mgs_fused, nb, NTV, 0, c.stream, n, i,
+                                      (const double*)basis, w, basis + (size_t)(i + 1) * n,
+                                      as<double>(g->mgs_part), hd, as<unsigned>(g->mgs_bar));
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      fused = false;
+    } else {
+      count_launch();
+    }
+  }
+  if (!fused) {
   for (int pass = 0; pass < 2; ++pass)
     for (int j = 0; j <= i; ++j) {
       double* c = hd + pass * (i + 1) + j;

@@ -191,16 +191,42 @@ class DeviceState:
             self.handle = None
 
     # -- sharding over ranks ---------------------------------------------------------
-    def set_sharding(self, rank, world, group=None):
-        """Own the contiguous band range of `rank` (k blocks stay whole when N_k >= world)."""
+    def set_sharding(self, rank, world, group=None, transport=None):
+        """Own the contiguous band range of `rank` (k blocks stay whole when N_k >= world).
+
+        transport "nccl" (default; env PWB_DIST_BACKEND): the library's own NCCL
+        communicator, whose unique id rank 0 creates and `group` broadcasts once;
+        anything else (the gloo shared-GPU control-flow check) sums the packet with
+        torch.distributed instead.  Either way a chi0 apply costs ONE all-reduce.
+        """
+        import os
+        torch = torch_mod()
         self.shard = shard_range(self.nocc, rank, world)
-        self.comm = (rank, world, group) if world > 1 else None
+        self.comm = None
+        if world <= 1:
+            return
+        import torch.distributed as dist
+        transport = transport or os.environ.get("PWB_DIST_BACKEND", "nccl")
+        if transport == "nccl":
+            uid = ctypes.create_string_buffer(128)
+            if rank == 0:
+                _lib.check(self._lib.pwb_comm_unique_id(uid), "pwb_comm_unique_id")
+            obj = [uid.raw if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+            _lib.check(self._lib.pwb_comm_init(self.handle, uid, rank, world), "pwb_comm_init")
+        n = ctypes.c_longlong(0)
+        _lib.check(self._lib.pwb_chi0_packet_size(self.handle, ctypes.byref(n)))
+        self.layout = packet_layout(self.grid.n_g, self.nband, abs(self.fp_den) > self.fp_thresh)
+        assert n.value == self.layout["size"], "packet layout out of sync with the library"
+        self._packet = torch.empty(n.value, dtype=torch.float64, device=self.device)
+        self.comm = (rank, world, group, transport)
 
     def chi0(self, dv_t, tol):
         """drho (device tensor) and per-(k, n) iteration counts of the local shard.
 
         With sharding active the result is already all-reduced over ranks, and
-        the returned iteration counts cover the whole (k, n) list (all-gathered).
+        the returned iteration counts cover the whole (k, n) list.
         """
         self.chi0_begin(dv_t)
         return self.chi0_finish(tol)
@@ -212,33 +238,53 @@ class DeviceState:
         self._dv_pending = dv_t   # keep the input alive until finish
         _lib.check(self._lib.pwb_chi0_begin(self.handle, b0, b1, ptr(dv_t), ptr(self._fsum)),
                    "chi0_begin")
-        if self.comm is not None and abs(self.fp_den) > self.fp_thresh:
-            import torch.distributed as dist
-            dist.all_reduce(self._fsum[:1], group=self.comm[2])   # global delta eps_F (metals)
 
     def chi0_finish(self, tol):
-        """Sternheimer solves + delta rho accumulation of the pending chi0."""
+        """Sternheimer solves + delta rho accumulation of the pending chi0.
+
+        Sharded: the rank's solves and accumulation (delta eps_F = 0), ONE
+        all-reduce of the packet [drho | C(r) | sum w f' delta eps | failures |
+        iterations], then drho -= delta eps_F C(r) on the device (pwb200.h)."""
         torch = torch_mod()
         tol = np.ascontiguousarray(tol, dtype=float)
         drho = torch.empty(self.grid.n_g, dtype=torch.float64, device=self.device)
         b0, b1 = self.shard
-        its_local = np.zeros(max(b1 - b0, 1), dtype=np.int32)
         tl = np.ascontiguousarray(tol[b0:b1]) if b1 > b0 else np.zeros(1)
-        status = self._lib.pwb_chi0_finish(self.handle, ptr(self._fsum), _np_ptr(tl), ptr(drho),
-                                           _np_ptr(its_local))
+        hold = self._dv_pending   # noqa: F841 -- dv stays alive until the calls below return
         self._dv_pending = None
-        if self.comm is not None:
-            import torch.distributed as dist
-            group = self.comm[2]
-            dist.all_reduce(drho, group=group)
-            cnt = torch.zeros(self.nband, dtype=torch.int64, device=self.device)
-            cnt[b0:b1] = torch.from_numpy(its_local[: b1 - b0].astype(np.int64)).to(self.device)
-            dist.all_reduce(cnt, group=group)
-            its = cnt.cpu().numpy().astype(np.int32)
+        if self.comm is None:
+            its = np.zeros(max(b1 - b0, 1), dtype=np.int32)
+            status = self._lib.pwb_chi0_finish(self.handle, ptr(self._fsum), _np_ptr(tl),
+                                               ptr(drho), _np_ptr(its))
+            _lib.check(status, "chi0_finish")
+            return drho, its[: b1 - b0]
+        _, _, group, transport = self.comm
+        its = np.zeros(self.nband, dtype=np.int32)
+        resid = ctypes.c_double(np.nan)
+        if transport == "nccl":
+            status = self._lib.pwb_chi0_finish_sharded(
+                self.handle, ptr(self._fsum), _np_ptr(tl), ptr(self._packet), ptr(drho),
+                _np_ptr(its), ctypes.byref(resid))
         else:
-            its = its_local[: b1 - b0]
+            import torch.distributed as dist
+            _lib.check(self._lib.pwb_chi0_finish_local(self.handle, ptr(self._fsum), _np_ptr(tl),
+                                                       ptr(self._packet)), "chi0_finish_local")
+            dist.all_reduce(self._packet, group=group)
+            status = self._lib.pwb_chi0_reduce_apply(self.handle, ptr(self._packet), ptr(drho),
+                                                     _np_ptr(its), ctypes.byref(resid))
         _lib.check(status, "chi0_finish")
         return drho, its
+
+
+def packet_layout(n_g, nband, metal):
+    """Offsets (in doubles) of the per-chi0 all-reduce packet (pwb200.h,
+    pwb_chi0_finish_local): slices drho / fermi (C(r), metals only) / iters /
+    resid, scalar offsets fsum / nfail, and the total size."""
+    base = n_g * (2 if metal else 1)
+    return {"drho": slice(0, n_g), "fermi": slice(n_g, 2 * n_g) if metal else None,
+            "fsum": base, "nfail": base + 1, "iters": slice(base + 2, base + 2 + nband),
+            "resid": slice(base + 2 + nband, base + 2 + 2 * nband),
+            "size": base + 2 + 2 * nband}
 
 
 def shard_range(nocc, rank, world):

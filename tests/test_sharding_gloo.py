@@ -1,12 +1,15 @@
 """Multi-rank decomposition of chi0 on CPU (gloo, world size 2).
 
 The B200 path shards the (k, n) Sternheimer solves over ranks
-(`DeviceState.set_sharding` -> `shard_range`), all-reduces the Fermi-level
-numerator sum_k w_k sum_n f'_nk d eps_nk before the occupation term
-(metals), and all-reduces the partial delta rho once per chi0 apply.  This
-test runs exactly that decomposition with the CPU oracle's per-band pieces
-on two gloo ranks and checks it against the unsharded oracle chi0 (the same
-sum in a different order).
+(`DeviceState.set_sharding` -> `shard_range`); each rank accumulates its
+bands with delta eps_F = 0 into ONE packet laid out by
+`device.packet_layout` ([drho | C(r) = sum w f' |psi|^2 | sum w f' d eps |
+failed rows | iterations | failed residuals]), the packets are summed by ONE
+all-reduce per chi0 apply, and the global Fermi shift is folded in
+afterwards (drho -= d eps_F C(r), the device kernel k_fermi_apply).  This
+test runs exactly that protocol with the CPU oracle's per-band pieces on two
+gloo ranks and checks it against the unsharded oracle chi0 (the same sum in
+a different order), and that a failure on one rank reaches every rank.
 """
 
 import os
@@ -54,11 +57,19 @@ def _pieces(ks, dv, tols, bands):
     return out
 
 
+def fold_packet(packet, layout, fp_den):
+    """k_fermi_apply's arithmetic: sum of partials - (sum w f' d eps / sum w f') C(r)."""
+    drho = packet[layout["drho"]]
+    if layout["fermi"] is None:
+        return drho
+    return drho - (packet[layout["fsum"]] / fp_den) * packet[layout["fermi"]]
+
+
 def _worker(rank, world, port, result_file):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2505_02319_b200.device import shard_range
+    from paper_2505_02319_b200.device import packet_layout, shard_range
     ks, z = _k_state()
     nocc = [b.n_occ for b in ks.blocks]
     b0, b1 = shard_range(nocc, rank, world)
@@ -67,22 +78,30 @@ def _worker(rank, world, port, result_file):
     tols = np.full(ntot, 1e-12)
     pieces = _pieces(ks, dv, tols, range(b0, b1))
     w = ks.weights
-    # global delta eps_F: one all-reduce of the numerator (denominator known on the host)
-    num = torch.tensor([sum(w[p["k"]] * p["fp"] * p["de"] for p in pieces.values())],
-                       dtype=torch.float64)
-    dist.all_reduce(num)
     den = sum(w[k] * float(blk.fprime_occ().sum()) for k, blk in enumerate(ks.blocks))
     thresh = 1e-14 * sum(wk * n for wk, n in zip(w, nocc))
-    de_f = float(num.item()) / den if abs(den) > thresh else 0.0
-    drho = np.zeros(ks.grids.n_g)
-    for p in pieces.values():
-        df = p["fp"] * (p["de"] - de_f)
-        drho += w[p["k"]] * (2.0 * p["f"] * (p["psi_r"].conj() * p["dphi_r"]).real
-                             + df * np.abs(p["psi_r"]) ** 2)
-    t = torch.from_numpy(drho)
-    dist.all_reduce(t)                      # the one delta-rho all-reduce per chi0 apply
+    metal = abs(den) > thresh
+    assert metal   # the fixture exercises the Fermi-level fold
+    lay = packet_layout(ks.grids.n_g, ntot, metal)
+    pk = np.zeros(lay["size"])
+    for gb, p in pieces.items():   # this rank's rows, delta eps_F = 0
+        wk = w[p["k"]]
+        pk[lay["drho"]] += wk * (2.0 * p["f"] * (p["psi_r"].conj() * p["dphi_r"]).real
+                                 + p["fp"] * p["de"] * np.abs(p["psi_r"]) ** 2)
+        pk[lay["fermi"]] += wk * p["fp"] * np.abs(p["psi_r"]) ** 2
+        pk[lay["fsum"]] += wk * p["fp"] * p["de"]
+        pk[lay["iters"]][gb] = 1.0
+    if rank == 1:   # a failed row on one rank only
+        pk[lay["nfail"]] = 1.0
+        pk[lay["resid"]][b0] = 3.5e-3
+    t = torch.from_numpy(pk)
+    dist.all_reduce(t)                      # the ONE all-reduce per chi0 apply
+    red = t.numpy()
+    # every rank sees every row's count and the other rank's failure
+    assert np.all(red[lay["iters"]] == 1.0)
+    assert red[lay["nfail"]] == 1.0 and red[lay["resid"]][b0 if rank == 1 else b1] == 3.5e-3
     if rank == 0:
-        np.save(result_file, t.numpy())
+        np.save(result_file, fold_packet(red, lay, den))
     dist.barrier()
     dist.destroy_process_group()
 
