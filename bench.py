@@ -35,9 +35,9 @@ METRIC = "H*psi band-applies/s per inexact-GMRES delta_rho solve"
 UNIT = "band-applies/s"
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0
-# DRAM bytes per band-apply of the H-apply kernels from the committed ncu --set full
-# capture (profiles/r01_ncu_happly_summary.txt), for roofline.traffic
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+# DRAM bytes per unit (band-apply / projected row) of the hot kernel groups from the
+# committed ncu --set full captures, keyed by cube, for roofline.traffic
+TRAFFIC_FILES = [os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")]
 
 
 def parse():
@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--config", type=int, default=4)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=15.0)
@@ -69,28 +69,15 @@ def dist_env():
 # workload construction (setup, not timed)
 
 def build_workload(cfg):
-    """(gs, dv0 numpy, params) for a BASELINE config, seeded.
-
-    The ground state is generated on the GPU (LOBPCG + k-point SCF, setup, not
-    timed); dV0 is drawn from the same generator after the wells.
-    """
-    from paper_2505_02319_b200 import synth
-    from paper_2505_02319_b200.groundstate import GaussianWell, ModelSpec
-    from paper_2505_02319_b200.lobpcg import run_scf_gpu
-    from paper_2505_02319_b200.pwbasis import Lattice
-    if cfg not in (0, 1, 2, 4):
-        raise SystemExit(f"config {cfg} is not a Dyson-solve workload")
-    spec = synth.build_model(cfg, Lattice, GaussianWell, ModelSpec)
-    gs = run_scf_gpu(spec["model"], kgrid=spec["params"]["kgrid"], tol=1e-9,
-                     n_states=spec["params"].get("n_states"))
-    g = gs.grids
-    dv0 = synth.smoothed_noise(g.g2_cube, g.cube_dims, spec["rng"])
-    return gs, dv0, spec["params"]
+    """(gs, dv0 numpy, params) for a BASELINE config, seeded: the ground
+    state from the GPU SCF (setup, not timed), dV0 drawn from the same generator
+    after the wells (paper_2505_02319_b200.cli.make_workload)."""
+    from paper_2505_02319_b200.cli import make_workload
+    return make_workload(cfg)
 
 
 def workload_desc(cfg, gs, params):
-    from paper_2505_02319_b200.device import state_blocks
-    blocks, _ = state_blocks(gs)
+    blocks = list(gs.blocks) if hasattr(gs, "blocks") else [gs]
     g = blocks[0].grids
     return {
         "workload": f"BASELINE configs[{cfg}]: full inexact-GMRES Dyson solve (RHS + GMRES)",
@@ -169,45 +156,63 @@ def peaks():
         return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
-def roofline_from_profile(prof, gs):
-    """Dominant kernel group of the solve and its achieved HBM bandwidth.
+def _traffic(cube, group):
+    """Per-unit DRAM bytes of a kernel group from a committed ncu --set full capture
+    (profiles/*_ncu_traffic.json, keyed by cube), or (None, None)."""
+    key = "x".join(str(int(d)) for d in cube)
+    for path in TRAFFIC_FILES:
+        try:
+            with open(path) as fh:
+                t = json.load(fh)
+        except (OSError, ValueError):
+            continue
+        ent = t.get(key, {}).get(group)
+        if ent:
+            return ent["dram_bytes_per_unit"], ent["capture"]
+    return None, None
 
-    The H apply's algorithmic bytes per band-apply are SURVEY.md 8(d)'s
-    3-pass full-cube model B_H = 64 N_g + 32 N_b; the pruned-plane traffic
-    of this implementation is reported beside it.
+
+def _shares(prof):
+    shares = {k: v[0] for k, v in prof.items()}
+    total = sum(shares.values())
+    return shares, {k: (v / total if total > 0 else 0.0) for k, v in shares.items()}
+
+
+def roofline_from_profile(prof, gs):
+    """HBM roofline of the H apply over the profiled solve.
+
+    Algorithmic bytes per band-apply: SURVEY.md 8(d)'s 3-pass full-cube model
+    B_H = 64 N_g + 32 N_b.  This implementation prunes the zero x planes, so
+    its DRAM traffic is below B_H; `traffic` (ncu dram bytes of the same
+    kernels per launch) and `frac_dram` (that traffic / launch time / peak)
+    report the fraction on the bytes actually moved.
     """
     from paper_2505_02319_b200.device import state_blocks
     blocks, _ = state_blocks(gs)
     g = blocks[0].grids
     n_g, n_b = g.n_g, int(np.mean([b.grids.n_b for b in blocks]))
     peak, how = peaks()
-    shares = {k: v[0] for k, v in prof.items()}
-    total = sum(shares.values())
+    shares, frac = _shares(prof)
     ms, count, units = prof["ham_apply"]
     b_h = 64.0 * n_g + 32.0 * n_b
     avg_ms = ms / max(count, 1)
     bands = units / max(count, 1)
-    bytes_per_launch = b_h * bands
-    achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
-    traffic, traffic_src = None, None
-    try:
-        with open(TRAFFIC_FILE) as fh:
-            t = json.load(fh)["ham_apply"]
-        if n_g == 48 ** 3:   # the capture is of this grid
-            traffic = t["dram_bytes_per_band_apply"] * bands
-            traffic_src = t["capture"]
-    except (OSError, KeyError, ValueError):
-        pass
-    return {
+    achieved = b_h * bands / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
+    per, src = _traffic(g.cube_dims, "ham_apply")
+    traffic = per * bands if per else None
+    out = {
         "kernel": "ham_apply (plane_inv + pencil V(r) + plane_fwd, one batched H psi)",
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+        "frac": achieved / peak, "traffic": traffic, "traffic_source": src,
         "peak_source": how,
         "algorithmic_bytes_per_band_apply": b_h,
-        "avg_launch_ms": avg_ms, "bands_per_launch": units / max(count, 1),
-        "share_of_kernel_time": {k: (v / total if total > 0 else 0.0) for k, v in shares.items()},
-        "kernel_ms": shares,
+        "avg_launch_ms": avg_ms, "bands_per_launch": bands,
+        "share_of_kernel_time": frac, "kernel_ms": shares,
     }
+    if traffic:
+        out["achieved_dram"] = traffic / (avg_ms * 1e-3) / 1e9
+        out["frac_dram"] = out["achieved_dram"] / peak
+    return out
 
 
 def projector_roofline(prof, gs, peak_fp64):
@@ -223,15 +228,27 @@ def projector_roofline(prof, gs, peak_fp64):
     f_row = 16.0 * float(np.sum(nocc * nb * nocc) / np.sum(nocc))
     ms, count, units = prof["projector"]
     achieved = f_row * units / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    shares, frac = _shares(prof)
+    per, src = _traffic(blocks[0].grids.cube_dims, "projector")
+    rows = units / max(count, 1)
     return {"kernel": "projector Q X (k_proj_coef + k_proj_apply), all CG calls of one solve",
             "bound": "tensor", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s (FP64)",
-            "frac": achieved / peak_fp64, "traffic": None,
-            "peak_source": "measured live: cuBLAS DGEMM 8192^3 best of 5",
+            "frac": achieved / peak_fp64, "traffic": per * rows if per else None,
+            "traffic_source": src,
+            "peak_source": "measured live: cuBLAS DGEMM 8192^3 best of 5 (MEASURED_PEAKS.json "
+                           "has no FP64 entry)",
             "algorithmic_flop_per_row": f_row, "rows": int(units), "launch_pairs": int(count),
-            "avg_rows_per_call": units / max(count, 1)}
+            "avg_rows_per_call": rows, "avg_launch_ms": ms / max(count, 1),
+            "share_of_kernel_time": frac, "kernel_ms": shares}
 
 
-def oracle_sample(gs, dv0, params, budget_s, threads=1):
+def dominant_roofline(ham, proj):
+    """The roofline object of the kernel group with the larger share of the solve."""
+    sh = ham["share_of_kernel_time"]
+    return dict(proj) if sh.get("projector", 0) >= sh.get("ham_apply", 0) else dict(ham)
+
+
+def oracle_sample(og, dv0, params, budget_s, threads=1):
     """Bounded CPU sample of the workload: the oracle's RHS + Sternheimer solves of
     the first (k, n) pairs at the solve's iteration-0 tolerances, band-applies/s.
 
@@ -246,7 +263,6 @@ def oracle_sample(gs, dv0, params, budget_s, threads=1):
     from oracle import model as om
     from oracle import outer as oo
     from oracle import response as orsp
-    og = to_oracle(gs)
     spec = oo.parse(params["strategy"], params["tau"], params["m"])
     nrm = float(np.linalg.norm(dv0))
     tols = od.tolerance_vector(og, spec, 0, kv_norm=nrm, rhs_norm=1.0)
@@ -288,7 +304,7 @@ def cpu_baseline(gs, dv0, params, budget_s):
     from oracle import model as om
     from oracle import outer as oo
     if hasattr(gs, "blocks") or gs.grids.n_g > 100000:
-        v, sample = oracle_sample(gs, dv0, params, budget_s)
+        v, sample = oracle_sample(to_oracle(gs), dv0, params, budget_s)
         return {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
     og = to_oracle(gs)
     spec = oo.parse(params["strategy"], params["tau"], params["m"])
@@ -364,31 +380,22 @@ class _MicroState:
         return np.zeros(self.n_occ)
 
 
-def run_microbench(args):
-    """configs[3]: 96^3 cube, 256 random orthonormal bands (Phi = the bands), V ~ U(-1,1)
-    smoothed; eps_n = Re <psi_n, H psi_n>; step = one batched projected-CG iteration of
-    the 256 Sternheimer rows rhs_n = -Q(V psi_n) through the C-ABI (pwb_sternheimer:
-    init projection + one iteration = 1 batched H apply + 5 Q, the reference op
-    sequence, sternheimer.py:59-91).  Separately timed: the batched H apply alone
-    (HBM roofline) and one Q on the 256 rows (FP64 roofline)."""
-    import ctypes
-
+def micro_setup(dev):
+    """configs[3] inputs on `dev`: 96^3 grid, 256 random orthonormal bands (= Phi), V ~
+    U(-1,1) smoothed, eps_n = Re <psi_n, H psi_n> (GPU H), rhs_n = -Q (V psi_n) as device
+    rows, and the device state the Sternheimer step runs on."""
     import torch
 
     from paper_2505_02319_b200 import _lib, ops, synth
     from paper_2505_02319_b200.device import device_state, ptr
     from paper_2505_02319_b200.pwbasis import Lattice, build_grids
-    world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     p, _, rng = synth.model_parameters(3)
     g = build_grids(Lattice.from_vectors(*synth.cell_vectors(p["cell"])), p["e_cut"])
-    nb = 256
+    nb = p["n_bands"]
     phi = synth.random_orthonormal(rng, g.n_b, nb)
     v = synth.smoothed_uniform(g.g2_cube, g.cube_dims, rng)
     eps = np.zeros(nb)
-    ms0 = _MicroState(g, phi, eps, v)
-    ds = device_state(ms0)
+    ds = device_state(_MicroState(g, phi, eps, v))
     dg = ds.grid
     vt = torch.from_numpy(v).to(dev)
     psi = dg.pack(list(phi.T))
@@ -400,17 +407,52 @@ def run_microbench(args):
     # rhs_n = -Q (V psi_n): V psi in the sphere basis, then the projector
     rhs = -ops.to_fourier_many_dev(dg, ops.to_real_many_dev(dg, psi) * vt[None, :])
     _lib.check(lib.pwb_project_out(ds.handle, 0, nb, ptr(rhs)), "project_out")
-    bands = np.arange(nb, dtype=np.int32)
-    tol = np.full(nb, 1e300)                     # every row stops after its one iteration
-    x = torch.zeros_like(rhs)
+    return dict(p=p, g=g, phi=phi, v=v, vt=vt, eps=eps, ms=ms, ds=ds, dg=dg, psi=psi, rhs=rhs,
+                nb=nb)
+
+
+def micro_step(m, x, rhs=None, tol_value=1e300):
+    """One pwb_sternheimer call on the 256 rows of configs[3] (init Q + one iteration =
+    1 batched H apply + 5 Q when tol_value is unreachable-high): returns (its, res)."""
+    import ctypes
+
+    from paper_2505_02319_b200 import _lib
+    from paper_2505_02319_b200.device import ptr
+    nb = m["nb"]
+    bands = m.setdefault("bands", np.arange(nb, dtype=np.int32))
+    tol = np.full(nb, tol_value)
     its = np.zeros(nb, dtype=np.int32)
     res = np.zeros(nb)
+    _lib.check(_lib.load().pwb_sternheimer(
+        m["ds"].handle, nb, ctypes.c_void_p(bands.ctypes.data),
+        ptr(m["rhs"] if rhs is None else rhs), ctypes.c_void_p(tol.ctypes.data), 0, ptr(x),
+        ctypes.c_void_p(its.ctypes.data), ctypes.c_void_p(res.ctypes.data)), "sternheimer")
+    return its, res
+
+
+def run_microbench(args):
+    """configs[3]: 96^3 cube, 256 random orthonormal bands (Phi = the bands), V ~ U(-1,1)
+    smoothed; eps_n = Re <psi_n, H psi_n>; step = one batched projected-CG iteration of
+    the 256 Sternheimer rows rhs_n = -Q(V psi_n) through the C-ABI (pwb_sternheimer:
+    init projection + one iteration = 1 batched H apply + 5 Q, the reference op
+    sequence, sternheimer.py:59-91).  Separately timed: the batched H apply alone
+    (HBM roofline) and one Q on the 256 rows (FP64 roofline)."""
+    import torch
+
+    from paper_2505_02319_b200 import _lib
+    from paper_2505_02319_b200.device import ptr
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    m = micro_setup(dev)
+    g, nb, ds, dg, psi, vt, rhs, p = (m[k] for k in ("g", "nb", "ds", "dg", "psi", "vt", "rhs",
+                                                      "p"))
+    lib = _lib.load()
+    x = torch.zeros_like(rhs)
+    its = np.zeros(nb, dtype=np.int32)
 
     def step():
-        _lib.check(lib.pwb_sternheimer(ds.handle, nb, ctypes.c_void_p(bands.ctypes.data),
-                                       ptr(rhs), ctypes.c_void_p(tol.ctypes.data), 0, ptr(x),
-                                       ctypes.c_void_p(its.ctypes.data),
-                                       ctypes.c_void_p(res.ctypes.data)), "sternheimer")
+        its[:] = micro_step(m, x)[0]
 
     def timed(fn, reps):
         torch.cuda.synchronize()
@@ -452,10 +494,7 @@ def run_microbench(args):
 
     def e2e_step():
         rhs_dev.copy_(pinned_in, non_blocking=True)
-        _lib.check(lib.pwb_sternheimer(ds.handle, nb, ctypes.c_void_p(bands.ctypes.data),
-                                       ptr(rhs_dev), ctypes.c_void_p(tol.ctypes.data), 0,
-                                       ptr(x), ctypes.c_void_p(its.ctypes.data),
-                                       ctypes.c_void_p(res.ctypes.data)), "sternheimer")
+        micro_step(m, x, rhs_dev)
         pinned_out.copy_(x, non_blocking=True)
     e2e_ms = timed(e2e_step, max(1, args.steps))
     peak_hbm, how = peaks()
@@ -493,41 +532,62 @@ def run_microbench(args):
     print(json.dumps(line))
 
 
+def reference_setup(cfg):
+    """Setup of the reference arm, outside the timed process: a child process runs
+    the GPU ground-state generator and writes the workload directory (archive +
+    dV0 + parameters, paper_2505_02319_b200.cli ground-state); this process only
+    reads it back with numpy (oracle.archive) and never loads the CUDA library."""
+    import tempfile
+    out = os.environ.get("PWB_REF_WORKLOAD") or tempfile.mkdtemp(prefix=f"pwb_ref_cfg{cfg}_")
+    cmd = [sys.executable, "-m", "paper_2505_02319_b200.cli", "ground-state", "--config",
+           str(cfg), "--out", out]
+    t0 = time.perf_counter()
+    if not os.path.exists(os.path.join(out, "workload.json")):
+        subprocess.run(cmd, check=True, cwd=ROOT, stdout=subprocess.DEVNULL)
+    setup_s = time.perf_counter() - t0
+    from oracle.archive import load_workload
+    og, dv0, params = load_workload(out)
+    return og, dv0, params, {"ground_state": "GPU SCF in a child process (" + " ".join(
+        ["python"] + cmd[1:]) + "), archive format 2 read back by oracle.archive (numpy)",
+        "setup_s": round(setup_s, 1), "workload_dir": out}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     import multiprocessing
-    gs, dv0, params = build_workload(args.config)
+    og, dv0, params, setup = reference_setup(args.config)
     ncores = len(os.sched_getaffinity(0))
-    if hasattr(gs, "blocks") or gs.grids.n_g > 100000:
+    common = {"metric": METRIC, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+              "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+              "scaling": "strong", "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic",
+              "config": dict(workload_desc(args.config, og, params),
+                             parallelism=f"kn-shard{args.gpus}"),
+              "reference": setup}
+    if hasattr(og, "blocks") or og.grids.n_g > 100000:
         vals = []
         t_all = time.perf_counter()
         for _ in range(args.warmup + args.steps):
-            v, sample = oracle_sample(gs, dv0, params, 10.0, threads=ncores)
+            v, sample = oracle_sample(og, dv0, params, 10.0, threads=ncores)
             vals.append(v)
         value = float(np.mean(vals[args.warmup:]))
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": (time.perf_counter() - t_all) / (args.warmup + args.steps) * 1e3,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f64/c128", "data": "synthetic",
-                "config": workload_desc(args.config, gs, params),
-                "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
-                                 "sample": "per step: " + sample +
-                                 f" (host has {multiprocessing.cpu_count()} cores)"},
-                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
+        line = dict(common, value=value,
+                    ms_per_step=(time.perf_counter() - t_all) / (args.warmup + args.steps) * 1e3,
+                    cpu_baseline={"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
+                                  "sample": "per step: " + sample +
+                                  f" (host has {multiprocessing.cpu_count()} cores)"},
+                    e2e={"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0})
         print(json.dumps(line))
         return
+    from threadpoolctl import threadpool_limits
+
     from oracle import dyson as od
     from oracle import model as om
     from oracle import outer as oo
-    from threadpoolctl import threadpool_limits
-
     from oracle import response as orsp
-    og = to_oracle(gs)
     spec = oo.parse(params["strategy"], params["tau"], params["m"])
     orsp.BAND_THREADS = cores = ncores
     with threadpool_limits(limits=1):
@@ -541,17 +601,13 @@ def run_reference(args):
             n_ham += om.ham_counter.value - start
         dt = time.perf_counter() - t0
     value = n_ham / dt
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic",
-            "config": workload_desc(args.config, gs, params),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full Dyson solves, oracle/ numpy port, "
-                                       f"{ncores}-thread band pool, BLAS 1 thread "
-                                       f"(host has {multiprocessing.cpu_count()} cores)"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    line = dict(common, value=value, ms_per_step=dt / args.steps * 1e3,
+                cpu_baseline={"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                              "sample": f"{args.steps} full Dyson solves, oracle/ numpy port, "
+                                        f"{ncores}-thread band pool, BLAS 1 thread "
+                                        f"(host has {multiprocessing.cpu_count()} cores)"},
+                e2e={"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": 0})
     print(json.dumps(line))
 
 
@@ -575,8 +631,10 @@ def main():
     from paper_2505_02319_b200.device import device_state
     from paper_2505_02319_b200.harness import solve_dyson
 
+    t_setup = time.perf_counter()
     gs, dv0, params = build_workload(args.config)
     ds = device_state(gs)
+    setup_s = time.perf_counter() - t_setup
     if world > 1:
         ds.set_sharding(rank, world, group)
     dev = torch.device("cuda", local)
@@ -678,13 +736,16 @@ def main():
             "dtype": "f64/c128", "data": "synthetic",
             "config": dict(workload_desc(args.config, gs, params), parallelism=f"kn-shard{world}"),
             "n_ham_per_solve": n_ham / args.steps, "gmres_iterations": iters,
+            "setup_s": round(setup_s, 1),
             "step_ms": [round(t, 3) for t in step_ms],
             "gpu_launches": int(launches), "clocks": clk, "e2e": e2e,
-            "roofline": roofline_from_profile(prof, gs),
+            "roofline": None,
+            "roofline_ham": roofline_from_profile(prof, gs),
             "roofline_projector": projector_roofline(prof, gs, fp64_peak(dev)),
             "kernel_ms_by_live_rows": {
                 cat: {f">={1 << b}": [round(ms, 2), n] for b, ms, n in rows}
                 for cat, rows in hist.items() if cat in ("ham_apply", "projector", "cg_vector")}}
+    line["roofline"] = dominant_roofline(line["roofline_ham"], line["roofline_projector"])
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(gs, dv0, params, args.cpu_budget)
     print(json.dumps(line))

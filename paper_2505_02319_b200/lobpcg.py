@@ -191,19 +191,35 @@ def run_scf_gpu(model, kgrid=(1, 1, 1), tol=1e-9, max_iter=200, kerker_alpha=0.8
     etol = 1e-4
     lda = model.xc == "lda_x"
     cx = (3.0 / np.pi) ** (1.0 / 3.0)
+    # states whose residual gates LOBPCG convergence: the occupied ones and the
+    # first empty one (eps_{N_occ+1}, groundstate.py:317-320); the rest of the
+    # block only accelerates convergence
+    n_check = min(n_states, model.n_electrons // 2 + 2)
+    vloc = None
     for it in range(max_iter):
         vh = kernel_apply_dev(kb.dg, False, rho, rho)     # Hartree: 4 pi/|G|^2 (G=0 -> 0)
         vloc = v_ext + vh
         if lda:
             vloc = vloc - cx * torch.clamp(rho, min=0.0) ** (1.0 / 3.0)
         vloc = vloc.contiguous()
-        eps, X, _ = lobpcg(kb, vloc, X, tol=etol)
+        eps, X, _ = lobpcg(kb, vloc, X, tol=etol, n_check=n_check)
         mu, _ = fermi_and_occupations(eps.reshape(-1), model.n_electrons, model.temperature,
-                                      model.smearing, np.repeat(wk, n_states))
+                                      model.smearing, np.repeat(wk, kb.nst))
         occ = occf((eps - mu) / model.temperature)
         nocc = [int(np.max(np.nonzero(o > model.occupation_threshold)[0])) + 1 for o in occ]
-        if max(nocc) + max(3, int(np.ceil(0.1 * max(nocc)))) > n_states:
-            raise NonConvergenceError("increase n_states: occupied states reach the block edge")
+        need = max(nocc) + max(3, int(np.ceil(0.1 * max(nocc))))
+        if need > kb.nst:
+            # the reference grows its state count and re-diagonalises the same
+            # potential (groundstate.py:366-372); here the block gains random
+            # directions orthogonal to the current one
+            if need > min(g.n_b for g in grids):
+                raise NonConvergenceError(f"basis too small: need {need} states")
+            kb, X = _grow(kb, X, need + 4, seed + it + 1)
+            n_states = kb.nst
+            if verbose:
+                print(f"gpu-scf {it:3d} block grown to {n_states} states", flush=True)
+            continue
+        n_check = min(kb.nst, max(nocc) + 1)
         rho_new = _density(kb, X, occ * wk[:, None])
         resid = rho_new - rho
         res = float(torch.linalg.vector_norm(resid).item()) * weight
@@ -211,9 +227,9 @@ def run_scf_gpu(model, kgrid=(1, 1, 1), tol=1e-9, max_iter=200, kerker_alpha=0.8
             print(f"gpu-scf {it:3d} res {res:.3e} mu {mu:+.6f} nocc {nocc} eig_tol {etol:.1e}",
                   flush=True)
         if res <= tol:
-            eps, X, eres = lobpcg(kb, vloc, X, tol=eig_tol)
+            eps, X, eres = lobpcg(kb, vloc, X, tol=eig_tol, n_check=n_check)
             mu, _ = fermi_and_occupations(eps.reshape(-1), model.n_electrons, model.temperature,
-                                          model.smearing, np.repeat(wk, n_states))
+                                          model.smearing, np.repeat(wk, kb.nst))
             occ = occf((eps - mu) / model.temperature)
             gs = _assemble(model, grids, X, eps, occ, mu, rho_new, vloc, res, wk, kfr)
             gs.eps_all = eps
@@ -221,6 +237,20 @@ def run_scf_gpu(model, kgrid=(1, 1, 1), tol=1e-9, max_iter=200, kerker_alpha=0.8
         etol = max(eig_tol, min(1e-4, 0.1 * res))
         rho = rho + damping * kerker_apply_dev(kb.dg, kerker_alpha, resid.contiguous())
     raise NonConvergenceError(f"GPU SCF did not reach {tol:.1e}", residual=res)
+
+
+def _grow(kb, X, n_new, seed):
+    """KBatch of n_new states whose first rows are X, the new ones random and
+    orthonormalised against them."""
+    torch = torch_mod()
+    kb2 = KBatch(kb.grids, n_new)
+    rng = np.random.default_rng(seed)
+    extra = n_new - kb.nst
+    R = rng.standard_normal((kb.nk, extra, kb.nbp)) + 1j * rng.standard_normal(
+        (kb.nk, extra, kb.nbp))
+    R = torch.from_numpy(R).to(X.device) * kb.mask[:, None, :]
+    R = R - torch.matmul(torch.matmul(R, X.conj().transpose(1, 2)), X)
+    return kb2, orthonormalise(torch.cat([X, R], 1))
 
 
 def _assemble(model, grids, X, eps, occ, mu, rho, vloc, res, wk, kfr):

@@ -8,11 +8,13 @@ import pytest
 from conftest import load_golden, product_gs
 
 
-def test_defaults_are_one_gpu_config1(monkeypatch):
+def test_defaults_are_one_gpu_config4(monkeypatch):
+    """The default workload is BASELINE configs[4], the config the metric's 1/2/4/8-GPU
+    series is quoted on (it fits one B200)."""
     import bench
     monkeypatch.setattr(sys, "argv", ["bench.py"])
     a = bench.parse()
-    assert (a.gpus, a.config, a.impl) == (1, 1, "ours")
+    assert (a.gpus, a.config, a.impl) == (1, 4, "ours")
     assert a.warmup >= 3 and a.steps >= 1
 
 
@@ -34,6 +36,19 @@ def test_roofline_objects_from_profile():
     assert q["bound"] == "tensor" and q["peak"] == 35.0
     f_row = 16.0 * gs.grids.n_b * gs.n_occ
     assert q["achieved"] == pytest.approx(f_row * 4000 / 20e-3 / 1e12)
+    # the line's `roofline` is the group with the larger share (the projector here)
+    d = bench.dominant_roofline(r, q)
+    assert d["bound"] == "tensor" and d["frac"] == q["frac"]
+    flip = {"projector": 0.1, "ham_apply": 0.5}
+    assert bench.dominant_roofline(dict(r, share_of_kernel_time=flip), q)["bound"] == "hbm"
+
+
+def test_traffic_lookup_by_cube():
+    import bench
+    per, src = bench._traffic((64, 64, 64), "ham_apply")
+    if per is not None:
+        assert per > 0 and "ncu" in src
+    assert bench._traffic((7, 7, 7), "ham_apply") == (None, None)
 
 
 def test_rank_environment(monkeypatch):

@@ -1,0 +1,193 @@
+"""Parity on the configurations the benchmark measures (seeded synthetic inputs,
+SURVEY App. A), GPU path vs the CPU oracle on the same ground state:
+
+* configs[1]: the full inexact-GMRES Dyson solve (RHS + GMRES) that bench.py
+  times -- GMRES iterations +-1, delta rho 1e-8 relative L2, the same
+  per-iteration Sternheimer tolerance schedule (north_star's bar);
+* configs[4]: chi0 restricted to k blocks (pwb_chi0_begin / finish on a block's
+  band range with the GLOBAL Fermi numerator of a full begin) against the
+  oracle's per-block chi0 with its own global delta eps_F, at the RHS
+  tolerances and at 1e-10;
+* configs[3]: the benchmarked pwb_sternheimer step (init Q + one projected-CG
+  iteration on all 256 rows) against the oracle's first CG step on 16 rows;
+* the GPU ground-state generator (lobpcg.run_scf_gpu) against the reference's
+  own run_scf ground states stored in the golden fixtures.
+
+The oracle runs with the reference's band thread pool on every host core
+(results are bitwise independent of the pool width, response.py:144-148).
+Ground states come from lobpcg.run_scf_gpu (bench.build_workload) and are
+fed to both sides.  Needs a B200."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2505_02319_b200 import _lib, build
+    build.build()
+    _lib.require_device()
+
+
+@pytest.fixture(scope="module")
+def pool():
+    """Oracle band pool on every host core, BLAS one thread per worker."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import response as orsp
+    old = orsp.BAND_THREADS
+    orsp.BAND_THREADS = max(1, len(os.sched_getaffinity(0)))
+    with threadpool_limits(limits=1):
+        yield orsp.BAND_THREADS
+    orsp.BAND_THREADS = old
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    import bench
+    return bench.build_workload(1)
+
+
+@pytest.fixture(scope="module")
+def cfg4():
+    import bench
+    return bench.build_workload(4)
+
+
+@pytest.mark.timeout(1800)
+def test_cfg1_full_dyson_solve_matches_oracle(cfg1, pool):
+    """The benchmarked configs[1] solve end to end (harness.py:215-292,
+    igmres.py:173-306): iterations +-1, delta rho 1e-8, tau schedule rtol 1e-6."""
+    import bench
+    from oracle import dyson as od
+    from oracle import outer as oo
+    from paper_2505_02319_b200.harness import solve_dyson
+    gs, dv0, p = cfg1
+    res = solve_dyson(gs, dv0, strategy=p["strategy"], tau=p["tau"], m=p["m"], xc=p["xc"])
+    ref = od.solve(bench.to_oracle(gs), dv0, oo.parse(p["strategy"], p["tau"], p["m"]),
+                   xc=p["xc"])
+    assert res.converged and ref.converged
+    assert abs(res.iterations - ref.iterations) <= 1
+    assert rel(res.solution.cpu().numpy(), ref.solution) < 1e-8
+    assert rel(res.rhs.cpu().numpy(), ref.rhs) < 1e-8
+    n = min(len(res.tolerance_schedule), len(ref.tolerance_schedule))
+    assert n >= ref.iterations
+    for got, want in zip(res.tolerance_schedule[:n], ref.tolerance_schedule[:n]):
+        np.testing.assert_allclose(got, want, rtol=1e-6)
+    assert abs(res.n_ham - ref.n_ham) <= 0.02 * ref.n_ham
+
+
+def _oracle_shifts(og, dv):
+    """Global delta eps_F of the oracle (sum_k w_k sum_n f' d eps / sum_k w_k sum_n f')."""
+    from oracle import response as orsp
+    num = den = 0.0
+    for blk, w in zip(og.blocks, og.weights):
+        b = blk.grids
+        pr = b.to_real_many(blk.phi_occ.T)
+        dvpsi = b.to_fourier_many(dv[None, :] * pr)
+        de = np.einsum("bn,nb->n", blk.phi_occ.conj(), dvpsi).real
+        fp = blk.fprime_occ()
+        num += w * float(fp @ de)
+        den += w * float(fp.sum())
+    thresh = 1e-14 * sum(w * blk.n_occ for blk, w in zip(og.blocks, og.weights))
+    return (num / den if abs(den) > thresh else 0.0), num, orsp
+
+
+@pytest.mark.timeout(1800)
+def test_cfg4_kblock_chi0_matches_oracle(cfg4, pool):
+    """configs[4] (64^3, 32 k-points, 2 119 (k, n) pairs): chi0 restricted to k blocks
+    (response.py:110-161 per k with the global delta eps_F) at the
+    RHS tolerances of the benchmarked solve and at 1e-10."""
+    import ctypes
+
+    import torch
+
+    import bench
+    from oracle import dyson as od
+    from oracle import outer as oo
+    from paper_2505_02319_b200 import _lib
+    from paper_2505_02319_b200.device import device_state, ptr
+    gs, dv0, p = cfg4
+    og = bench.to_oracle(gs)
+    assert len(og.blocks) == 32 and tuple(gs.grids.cube_dims) == (64, 64, 64)
+    nrm = float(np.linalg.norm(dv0))
+    dv = dv0 / nrm
+    de_f, num, orsp = _oracle_shifts(og, dv)
+    ds = device_state(gs)
+    lib = _lib.load()
+    dvt = torch.from_numpy(dv).cuda()
+    total = torch.zeros(2, dtype=torch.float64, device="cuda")
+    _lib.check(lib.pwb_chi0_begin(ds.handle, 0, ds.nband, ptr(dvt), ptr(total)))
+    assert abs(total[0].item() - num) <= 1e-10 * abs(num) + 1e-14   # global Fermi numerator
+    rhs_tols = od.tolerance_vector(og, oo.parse(p["strategy"], p["tau"], p["m"]), 0,
+                                   kv_norm=nrm, rhs_norm=1.0)
+    for k in (0, 13, 31):
+        blk, w = og.blocks[k], og.weights[k]
+        b0, b1 = ds.offsets[k], ds.offsets[k + 1]
+        for tols in (rhs_tols[b0:b1], np.full(b1 - b0, 1e-10)):
+            tl = np.ascontiguousarray(tols)
+            f = torch.zeros(2, dtype=torch.float64, device="cuda")
+            _lib.check(lib.pwb_chi0_begin(ds.handle, b0, b1, ptr(dvt), ptr(f)))
+            drho = torch.empty(ds.grid.n_g, dtype=torch.float64, device="cuda")
+            its = np.zeros(b1 - b0, dtype=np.int32)
+            _lib.check(lib.pwb_chi0_finish(ds.handle, ptr(total), ctypes.c_void_p(tl.ctypes.data),
+                                           ptr(drho), ctypes.c_void_p(its.ctypes.data)))
+            piece = orsp._chi0_block(blk, dv, tl, weight=w)
+            want = w * orsp._accumulate(blk, piece, piece["fp"] * (piece["de"] - de_f))
+            rits = np.array([r.cg_iterations for r in piece["results"]])
+            assert np.abs(its - rits).max() <= 1, (k, its, rits)
+            assert rel(drho.cpu().numpy(), want) < 1e-8, k
+
+
+def test_cfg3_sternheimer_step_matches_oracle(pool):
+    """The configs[3] step bench.py times (pwb_sternheimer on all 256 rows: init
+    Q + 1 H apply + 5 Q, sternheimer.py:59-91) vs the oracle's first CG step."""
+    import types
+
+    import torch
+
+    import bench
+    from oracle import basis as ob
+    from oracle import response as orsp
+    m = bench.micro_setup(torch.device("cuda", 0))
+    x = torch.zeros_like(m["rhs"])
+    its, res = bench.micro_step(m, x)
+    assert np.all(its == 1)
+    g, phi, v = m["g"], m["phi"], m["v"]
+    b = ob.make_basis(ob.Cell(g.lattice.a), m["p"]["e_cut"])
+    st = types.SimpleNamespace(grids=b, phi_occ=phi, eps=m["eps"])
+    xs = m["dg"].unpack(x)
+    rhs = m["dg"].unpack(m["rhs"])
+    rows = [0, 1, 2, 3, 31, 64, 77, 100, 127, 128, 150, 200, 222, 253, 254, 255]
+    for n in rows:
+        want_rhs = -orsp.project_out(phi, b.to_fourier(v * b.to_real(phi[:, n])))
+        assert rel(rhs[n], want_rhs) < 1e-11, n
+        r = orsp.sternheimer(st, v, n, want_rhs, 1e300)
+        assert r.cg_iterations == 1
+        assert rel(xs[n], r.solution) < 1e-10, n
+        assert abs(res[n] - r.final_residual_norm) <= 1e-10 * r.final_residual_norm
+
+
+@pytest.mark.parametrize("name,kw", [("dyson_cfg0.npz", {}),
+                                     ("metal.npz", {"damping": 0.3, "max_iter": 400})])
+def test_gpu_scf_matches_reference_run_scf(name, kw):
+    """lobpcg.run_scf_gpu vs the reference's dense run_scf (groundstate.py:333-394) on
+    the ground states stored in the golden fixtures: N_occ, eigenvalues, Fermi level
+    and density."""
+    from conftest import product_gs
+    from paper_2505_02319_b200.lobpcg import run_scf_gpu
+    z = load_golden(name)
+    ref = product_gs(z)
+    # same SCF settings as the golden run (tests/golden/gen_golden.py)
+    gs = run_scf_gpu(ref.model, tol=1e-11, eig_tol=1e-10, **kw)
+    assert gs.n_occ == ref.n_occ
+    k = ref.n_occ + 1
+    np.testing.assert_allclose(gs.eps[:k], ref.eps[:k], rtol=0, atol=1e-8)
+    assert abs(gs.fermi_level - ref.fermi_level) <= 1e-8
+    assert rel(gs.rho, ref.rho) < 1e-8

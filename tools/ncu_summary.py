@@ -15,7 +15,13 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
-        "lts__t_bytes.sum"]
+        "lts__t_bytes.sum",
+        "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_subpipe_dmma.sum",
+        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "launch__grid_size", "launch__block_size"]
 STALLS = ["barrier", "short_scoreboard", "long_scoreboard", "mio_throttle", "math_pipe_throttle",
           "wait", "not_selected", "selected", "lg_throttle", "dispatch_stall", "tex_throttle"]
 
