@@ -203,6 +203,13 @@ int pwb_project_host(int nb, int nocc, const double* phi_host, int ncol, double*
 /* ---- dense vector helpers for the device-resident inexact GMRES ----------
  * (igmres.py:86-114): deterministic reductions, scalars stay on device.      */
 int pwb_vec_dot(pwb_grid* grid, int n, const double* x, const double* y, double* out_dev);
+/* out <- a x + b y (y may be NULL: out <- a x); products and sum rounded
+ * separately, i.e. numpy's `a * x + b * y` (v - |Kv| chi0, response.py:187;
+ * b - E x0, igmres.py:233)                                                   */
+int pwb_vec_axpby(pwb_grid* grid, long long n, double a, const double* x, double b,
+                  const double* y, double* out);
+/* out <- x / d (numpy's `x / d`: Kv/|Kv|, response.py:181; r0/beta, igmres.py:64) */
+int pwb_vec_div(pwb_grid* grid, long long n, const double* x, double d, double* out);
 /* y <- y + a x  (a host scalar) */
 int pwb_vec_axpy(pwb_grid* grid, int n, double a, const double* x, double* y);
 /* Arnoldi MGS step with one re-orthogonalisation pass (igmres.py:86-103):

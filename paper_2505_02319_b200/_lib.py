@@ -65,6 +65,9 @@ SIGNATURES = {
     "pwb_profile_hist": (ctypes.c_int, [_vp, _vp]),
     "pwb_vec_dot": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
     "pwb_vec_axpy": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_double, _vp, _vp]),
+    "pwb_vec_axpby": (ctypes.c_int, [_vp, ctypes.c_longlong, ctypes.c_double, _vp,
+                                     ctypes.c_double, _vp, _vp]),
+    "pwb_vec_div": (ctypes.c_int, [_vp, ctypes.c_longlong, _vp, ctypes.c_double, _vp]),
     "pwb_arnoldi_mgs": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
     "pwb_vec_combine": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "pwb_chi0_packet_size": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_longlong)]),

@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpwb200.so")
-SOURCES = ["grid.cu", "fft_kernels.cu", "proj.cu", "state.cu", "cg.cu", "chi0.cu", "vec.cu", "comm.cu"]
+SOURCES = ["grid.cu", "fft_kernels.cu", "proj.cu", "state.cu", "cg.cu", "chi0.cu", "vec.cu", "comm.cu", "projw.cu"]
 HEADERS = ["common.cuh", "fft_engine.cuh", "grid.cuh", "proj.cuh", "state.cuh", "profile.cuh", "fft_static.cuh", "dispatch.cuh", "tma.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]

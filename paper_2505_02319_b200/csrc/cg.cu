@@ -217,7 +217,8 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
                                                   const int* __restrict__ row_k, IterCtl ctl) {
   pdl_wait();
   __shared__ int scan[1024];
-  __shared__ int kcnt[kMaxK], kstart[kMaxK], ktile[kMaxK];
+  __shared__ int kcnt[kMaxK], kstart[kMaxK], ktile[kMaxK], kwide[kMaxK];
+  __shared__ int wcarry;
   __shared__ int carry;
   const int tid = threadIdx.x;
   for (int k = tid; k < nk; k += 1024) kcnt[k] = 0;
@@ -250,21 +251,38 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
     ctl.rows2[na + j] = r + n;
   }
   if (tid == 0) {
-    int s = 0, t = 0;
+    int s = 0, t = 0, wt = 0;
     for (int k = 0; k < nk; ++k) {
       kstart[k] = s;
       ktile[k] = t;
+      kwide[k] = wt;
       s += kcnt[k];
       t += (kcnt[k] + kProjTileRows - 1) / kProjTileRows;
+      wt += (kcnt[k] + kProjWideRows - 1) / kProjWideRows;
     }
     ctl.hdr[0] = na;
     ctl.hdr[1] = t;
     ctl.hdr[2] = 2 * t;
     ctl.hdr[3] = 0;   // rows still iterating after this iteration (k_cg_resid counts)
+    ctl.hdr[8] = wt;  // wide tiles over rows / over the stacked rows
+    ctl.hdr[9] = 2 * wt;
     carry = t;
+    wcarry = wt;
   }
   __syncthreads();
-  const int ntile = carry;
+  const int ntile = carry, nwide = wcarry;
+  if (ctl.wa) {
+    for (int k = tid; k < nk; k += 1024) {
+      const int c = kcnt[k];
+      for (int j = 0; j * kProjWideRows < c; ++j) {
+        ProjTile tl{kstart[k] + kProjWideRows * j, min(kProjWideRows, c - kProjWideRows * j), k};
+        ctl.wa[kwide[k] + j] = tl;
+        ctl.wb[kwide[k] + j] = tl;
+        tl.row0 += na;
+        ctl.wb[nwide + kwide[k] + j] = tl;
+      }
+    }
+  }
   for (int k = tid; k < nk; k += 1024) {
     const int c = kcnt[k];
     for (int j = 0; j * kProjTileRows < c; ++j) {
@@ -307,13 +325,43 @@ ProjArgs proj_args(pwb_state* st) {
   a.ntiles = nullptr;
   a.phic = as<double2>(st->phic);
   a.phic_off = as<int>(st->phic_meta) + 2 * st->nk;
+  a.phiw = st->wide_ok ? as<double2>(st->phiw) : nullptr;
+  a.phiw_off = st->wide_ok ? as<int>(st->phiw_meta) + 2 * st->nk : nullptr;
   return a;
+}
+
+static bool use_wide(const pwb_state* st, const ProjPlan& pl, const int* ntiles,
+                     const int* wntiles) {
+  return st->wide_ok && projw_enabled() && plan_wide_tiles(pl) > 0 &&
+         (ntiles == nullptr) == (wntiles == nullptr);
+}
+
+int proj_coeffs_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* X,
+                    double2* part, double2* C, cudaStream_t s, const int* wntiles) {
+  if (use_wide(st, pl, a.ntiles, wntiles)) {
+    a.ntiles = wntiles;
+    return projw_coeffs(reinterpret_cast<const ProjTile*>(pl.dwtiles.ptr), (int)pl.wtiles.size(),
+                        plan_wide_tiles(pl), a, X, part, C,
+                        reinterpret_cast<unsigned*>(pl.wcounters.ptr), s);
+  }
+  return proj_coeffs(pl, a, X, part, C, s);
+}
+
+int proj_apply_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* C,
+                   const double2* Xin, double2* Y, double ca, double cb, const int* active,
+                   int band_mod, cudaStream_t s, const int* wntiles) {
+  if (use_wide(st, pl, a.ntiles, wntiles)) {
+    a.ntiles = wntiles;
+    return projw_apply(reinterpret_cast<const ProjTile*>(pl.dwtiles.ptr), (int)pl.wtiles.size(),
+                       plan_wide_tiles(pl), a, C, Xin, Y, ca, cb, active, band_mod, s);
+  }
+  return proj_apply(pl, a, C, Xin, Y, ca, cb, active, band_mod, s);
 }
 
 // Q X in place for the rows of a plan (masked by `active` when given)
 int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* active, int band_mod,
                  const int* rows, double2* part, double2* cmat, cudaStream_t s,
-                 const int* ntiles, int mult) {
+                 const int* ntiles, int mult, const int* wntiles) {
   ProjArgs a = proj_args(st);
   a.rows = rows;
   a.ntiles = ntiles;
@@ -332,8 +380,8 @@ int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* activ
     prof().end(PROF_Q, e, s, pl.nrows);
     return PWB_OK;
   }
-  PWB_TRY(proj_coeffs(pl, a, X, part, cmat, s));
-  PWB_TRY(proj_apply(pl, a, cmat, X, X, 1.0, -1.0, active, band_mod, s));
+  PWB_TRY(proj_coeffs_any(st, pl, a, X, part, cmat, s, wntiles));
+  PWB_TRY(proj_apply_any(st, pl, a, cmat, X, X, 1.0, -1.0, active, band_mod, s, wntiles));
   prof().end(PROF_Q, e, s, prof().rows_hint > 0 ? (long long)mult * prof().rows_hint : pl.nrows);
   return PWB_OK;
 }
@@ -370,8 +418,11 @@ int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands) {
     if (per_k[k] > 0) maxocc = std::max(maxocc, st->nocc[k]);
   }
   cg.max_tiles = std::max(1, maxt);
-  PWB_TRY(proj_plan_device(cg.pa, cg.max_tiles, maxocc, g->nbp));
-  PWB_TRY(proj_plan_device(cg.pb, 2 * cg.max_tiles, maxocc, g->nbp));
+  int maxw = 0;
+  for (int k = 0; k < st->nk; ++k) maxw += (per_k[k] + kProjWideRows - 1) / kProjWideRows;
+  const int wcap = st->wide_ok ? std::max(1, maxw) : 0;
+  PWB_TRY(proj_plan_device(cg.pa, cg.max_tiles, maxocc, g->nbp, wcap));
+  PWB_TRY(proj_plan_device(cg.pb, 2 * cg.max_tiles, maxocc, g->nbp, 2 * wcap));
   const size_t row = (size_t)g->nbp * sizeof(double2);
   PWB_TRY(cg.xr.ensure(2 * n * row));
   PWB_TRY(cg.z.ensure(n * row));
@@ -380,8 +431,10 @@ int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands) {
   PWB_TRY(cg.rhs.ensure(n * row));
   PWB_CUDA(cudaMemset(cg.ap.ptr, 0, n * row));
   PWB_CUDA(cudaMemset(cg.z.ptr, 0, n * row));
-  const size_t part = std::max({proj_part_elems(cg.plan1), proj_part_elems(cg.pa),
-                                proj_part_elems(cg.pb)});
+  size_t part = std::max({proj_part_elems(cg.plan1), proj_part_elems(cg.pa),
+                          proj_part_elems(cg.pb)});
+  if (st->wide_ok)
+    part = std::max({part, projw_part_elems(2 * wcap), projw_part_elems((int)cg.plan1.wtiles.size())});
   PWB_TRY(cg.part.ensure(part * sizeof(double2)));
   PWB_TRY(cg.cmat.ensure((size_t)2 * n * st->ldc * sizeof(double2)));
   const size_t nd = 5 * (size_t)n, ni = 4 * (size_t)n + 2;
@@ -398,12 +451,14 @@ int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands) {
   cg.s.maxit = ip + 2 * n;
   cg.s.row_k = ip + 3 * n;
   cg.s.counters = ip + 4 * n;
-  PWB_TRY(cg.ctl_buf.ensure((size_t)(8 + 3 * n) * sizeof(int)));
+  PWB_TRY(cg.ctl_buf.ensure((size_t)(kHdrInts + 3 * n) * sizeof(int)));
   cg.ctl.hdr = as<int>(cg.ctl_buf);
-  cg.ctl.rows = cg.ctl.hdr + 8;
+  cg.ctl.rows = cg.ctl.hdr + kHdrInts;
   cg.ctl.rows2 = cg.ctl.rows + n;
   cg.ctl.ta = reinterpret_cast<ProjTile*>(cg.pa.dtiles.ptr);
   cg.ctl.tb = reinterpret_cast<ProjTile*>(cg.pb.dtiles.ptr);
+  cg.ctl.wa = wcap > 0 ? reinterpret_cast<ProjTile*>(cg.pa.dwtiles.ptr) : nullptr;
+  cg.ctl.wb = wcap > 0 ? reinterpret_cast<ProjTile*>(cg.pb.dwtiles.ptr) : nullptr;
   std::vector<double> eps(n), ps(n);
   for (int i = 0; i < n; ++i) {
     eps[i] = st->eps[bands[i]];
@@ -438,7 +493,8 @@ static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s, bool re
   do {
     (void)launch_k(k_compact, 1, 1024, 0, s, n, st->nk, cg.s.active, cg.s.row_k, cg.ctl);
     count_launch();
-    if ((status = project_rows(st, cg.pa, p, cg.s.active, n, rows, part, cmat, s, cg.ctl.hdr + 1)))
+    if ((status = project_rows(st, cg.pa, p, cg.s.active, n, rows, part, cmat, s, cg.ctl.hdr + 1,
+                               1, cg.ctl.hdr + 8)))
       break;
     cudaEvent_t eh = prof().begin(s);
     if ((status = launch_plane_inv(g, n, bk, p, 1.0, W, rows, nact))) break;
@@ -446,21 +502,22 @@ static int enqueue_iteration(pwb_state* st, CgBatch& cg, cudaStream_t s, bool re
     if ((status = launch_plane_fwd(g, n, bk, W, 1.0, p, cg.s.eps, ap, rows, nact))) break;
     prof().end(PROF_H, eh, s, cg.prof_rows);
     if ((status = project_rows(st, cg.pa, ap, cg.s.active, n, rows, part, cmat, s,
-                               cg.ctl.hdr + 1)))
+                               cg.ctl.hdr + 1, 1, cg.ctl.hdr + 8)))
       break;
     cudaEvent_t ec = prof().begin(s);
     (void)launch_k(k_cg_alpha, n, NTC, 0, s, g->dev, cg.s, n, p, ap, xr, rows, nact);
     count_launch();
     prof().end(PROF_CG, ec, s, cg.prof_rows);
     if ((status = project_rows(st, cg.pb, xr, cg.s.active, n, cg.ctl.rows2, part, cmat, s,
-                               cg.ctl.hdr + 2, 2)))   // x and r rows together
+                               cg.ctl.hdr + 2, 2, cg.ctl.hdr + 9)))   // x and r rows together
       break;
     ec = prof().begin(s);
     (void)launch_k(k_cg_resid, n, NTC, 0, s, g->dev, cg.s, n, xr, z, rows, nact, cg.ctl.hdr + 3);
     count_launch();
     prof().end(PROF_CG, ec, s, cg.prof_rows);
     if (readback) cudaMemcpyAsync(cg.h_hdr, cg.ctl.hdr, 8 * sizeof(int), cudaMemcpyDeviceToHost, s);
-    if ((status = project_rows(st, cg.pa, z, cg.s.active, n, rows, part, cmat, s, cg.ctl.hdr + 1)))
+    if ((status = project_rows(st, cg.pa, z, cg.s.active, n, rows, part, cmat, s, cg.ctl.hdr + 1,
+                               1, cg.ctl.hdr + 8)))
       break;
     ec = prof().begin(s);
     (void)launch_k(k_cg_beta, n, NTC, 0, s, g->dev, cg.s, n, xr, z, p, rows, nact);

@@ -856,6 +856,22 @@ int proj_plan(ProjPlan& pl, const std::vector<int>& row_k, const std::vector<int
   pl.nrows = n;
   pl.mtiles = std::max(1, (maxocc + CM - 1) / CM);
   const int ntiles = (int)pl.tiles.size();
+  pl.wmax = 0;
+  projw_tiles(row_k, pl.wtiles);
+  if (!pl.wtiles.empty()) {   // wide list: small, uploaded synchronously
+    const size_t nw = pl.wtiles.size();
+    if (pl.dwtiles.bytes < nw * sizeof(ProjTile) || !pl.dwtiles.ptr)
+      PWB_TRY(pl.dwtiles.ensure(nw * sizeof(ProjTile)));
+    if (async) {
+      PWB_CUDA(cudaStreamSynchronize(st));
+    }
+    PWB_CUDA(cudaMemcpy(pl.dwtiles.ptr, pl.wtiles.data(), nw * sizeof(ProjTile),
+                        cudaMemcpyHostToDevice));
+    if (pl.wcounters.bytes < nw * sizeof(unsigned) || !pl.wcounters.ptr) {
+      PWB_TRY(pl.wcounters.ensure(nw * sizeof(unsigned)));
+      PWB_CUDA(cudaMemset(pl.wcounters.ptr, 0, nw * sizeof(unsigned)));
+    }
+  }
   pl.nsplit = nsplit_max(nbp);   // upper bound; the live count is chosen on the device
   PWB_TRY(pl.dtiles.ensure(std::max<size_t>(1, pl.tiles.size()) * sizeof(ProjTile)));
   if (!pl.tiles.empty()) {
@@ -885,10 +901,17 @@ size_t proj_part_elems(const ProjPlan& pl) {
   return (size_t)pl.nsplit * std::max(1, plan_tiles(pl)) * pl.mtiles * CM * TR;
 }
 
-int proj_plan_device(ProjPlan& pl, int max_tiles, int maxocc, int nbp) {
+int proj_plan_device(ProjPlan& pl, int max_tiles, int maxocc, int nbp, int wide_tiles) {
   PWB_TRY(proj_configure());
   if (nbp % KC) return fail(PWB_ERR_UNSUPPORTED, "projector: row stride not a multiple of 64");
   pl.tiles.clear();
+  pl.wtiles.clear();
+  pl.wmax = wide_tiles;
+  if (wide_tiles > 0) {
+    PWB_TRY(pl.dwtiles.ensure((size_t)wide_tiles * sizeof(ProjTile)));
+    PWB_TRY(pl.wcounters.ensure((size_t)wide_tiles * sizeof(unsigned)));
+    PWB_CUDA(cudaMemset(pl.wcounters.ptr, 0, (size_t)wide_tiles * sizeof(unsigned)));
+  }
   pl.max_tiles = max_tiles;
   pl.nrows = max_tiles * TR;
   pl.mtiles = std::max(1, (maxocc + CM - 1) / CM);

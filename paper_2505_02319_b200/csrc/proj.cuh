@@ -11,6 +11,11 @@ namespace pwb {
 constexpr int kProjTileRows = 16;   // rows per projector tile (<= 2 DMMA n-fragments)
 constexpr int kProjChunk = 64;      // sphere coefficients per pipeline chunk
 constexpr int kProjRowStride = kProjChunk + 4;   // padded smem / chunk-major row (double2)
+// wide tiles (projw.cu): up to 72 rows of one k block against all its <= 80 orbitals
+constexpr int kProjWideRows = 72;
+constexpr int kProjWideOcc = 80;
+constexpr int kProjWideChunk = 32;
+constexpr int kProjWideStride = kProjWideChunk + 4;
 
 struct ProjTile {
   int row0;   // first row of X in this tile
@@ -33,6 +38,10 @@ struct ProjArgs {
   // orbitals of one chunk are ONE contiguous TMA bulk copy
   const double2* phic;
   const int* phic_off;  // [nk], in double2
+  // the same with 32-coefficient chunks (wide tiles): block k, chunk c, orbital m at
+  // phiw + phiw_off[k] + (c * nocc[k] + m) * kProjWideStride
+  const double2* phiw;
+  const int* phiw_off;
 };
 
 // Build the chunk-major copy of the orbital rows phi [nband][nbp] (k blocks at
@@ -51,6 +60,10 @@ struct ProjPlan {
   size_t h_cap = 0;
   int nrows = 0, mtiles = 0, nsplit = 1, split_len = 0;
   int max_tiles = 0;   // > 0: tiles are produced on the device (capacity plan)
+  // wide tiles (projw.cu): host list (host plans) or device capacity (wmax > 0)
+  std::vector<ProjTile> wtiles;
+  DevBuf dwtiles, wcounters;
+  int wmax = 0;
   ~ProjPlan() {
     if (h_stage) cudaFreeHost(h_stage);
   }
@@ -60,9 +73,13 @@ inline int plan_tiles(const ProjPlan& pl) {
   return pl.max_tiles > 0 ? pl.max_tiles : (int)pl.tiles.size();
 }
 
-// capacity plan whose tile list (<= max_tiles entries) is written on the device;
-// launches cover max_tiles and CTAs beyond the device count ProjArgs::ntiles exit
-int proj_plan_device(ProjPlan& pl, int max_tiles, int maxocc, int nbp);
+// capacity plan whose tile list (<= max_tiles entries, <= wide_tiles wide ones) is
+// written on the device; launches cover the capacity and CTAs beyond the device
+// count ProjArgs::ntiles exit
+int proj_plan_device(ProjPlan& pl, int max_tiles, int maxocc, int nbp, int wide_tiles = 0);
+inline int plan_wide_tiles(const ProjPlan& pl) {
+  return pl.wmax > 0 ? pl.wmax : (int)pl.wtiles.size();
+}
 
 // build the tile list for rows with k blocks row_k; uploads synchronously, or
 // asynchronously on `st` when st != nullptr (staging buffer reused: the caller
@@ -84,5 +101,21 @@ int proj_apply(const ProjPlan& pl, ProjArgs a, const double2* C, const double2* 
 bool proj_small_fits(int ntiles, int nbp, int maxocc);
 int proj_small(const ProjPlan& pl, ProjArgs a, double2* X, const int* active, int band_mod,
                double2* part, double2* C, unsigned* flags, cudaStream_t st);
+
+// ---- wide-tile projector (projw.cu) ----------------------------------------------
+bool projw_enabled();
+// wide tiles (<= kProjWideRows rows of one k block) over rows with k blocks row_k
+int projw_tiles(const std::vector<int>& row_k, std::vector<ProjTile>& out);
+size_t projw_part_elems(int max_tiles);
+// C = Phi^H X over `cap` tiles (device count a.ntiles when set, else nt_host)
+int projw_coeffs(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* X,
+                 double2* part, double2* C, unsigned* counters, cudaStream_t st);
+// Y = ca X + cb Phi C
+int projw_apply(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* C,
+                const double2* Xin, double2* Y, double ca, double cb, const int* active,
+                int band_mod, cudaStream_t st);
+int projw_chunked(const double2* phi, int nbp, const std::vector<int>& off_host,
+                  const std::vector<int>& nocc_host, DevBuf& phiw, DevBuf& d_meta,
+                  cudaStream_t st);
 
 }  // namespace pwb

@@ -1,0 +1,497 @@
+// Wide-tile projector: Q X = X - Phi (Phi^H X) with one tile = up to 72 rows
+// of ONE k block against ALL its orbitals (<= 80), reference
+// sternheimer.py:28-30.  This is the shape of a Sternheimer batch at full
+// width (every occupied band of a k point iterates: rows_k = N_occ,k), where
+// the 16-row tiles of proj.cu re-stream Phi_k once per 16 rows and the X rows
+// once per 40-orbital block.  Here both operands cross L2 -> SM exactly once
+// per tile:
+//
+//   coef :  C[row][m] = sum_g conj(Phi_k[m][g]) X[row][g]
+//           stream-K over (tile, 32-coefficient chunk) units: every CTA of the
+//           persistent grid takes an equal contiguous run of units; a tile cut
+//           between CTAs leaves per-CTA partial C blocks that the last CTA to
+//           arrive sums in fixed CTA order (bitwise reproducible, one launch).
+//   apply:  Y[row][g] = a X[row][g] + b sum_m Phi_k[m][g] C[row][m]
+//           contiguous runs of (tile, chunk) units per CTA; the tile's C block
+//           stays in smem across its chunks.
+//
+// Operands arrive by TMA bulk copies (one copy for the chunk's Phi block from
+// the 32-wide chunk-major copy, one 512 B copy per gathered X row) into a
+// 2-stage smem ring driven by a producer warp and full/empty mbarriers.  The
+// nine consumer warps form a 3 x 3 grid over the output fragments (8 x 8
+// DMMA tiles, mma.sync.m8n8k4.f64 -> DMMA.8x8x4), so a warp reuses each
+// loaded A fragment across its n fragments and vice versa; complex products
+// use three real DMMAs (Gauss), as in proj.cu.
+#include <cstring>
+
+#include "proj.cuh"
+#include "tma.cuh"
+
+namespace pwb {
+
+constexpr int WR = kProjWideRows;    // rows per wide tile (9 n fragments)
+constexpr int WMO = kProjWideOcc;    // orbitals per k block (10 m fragments)
+constexpr int KW = kProjWideChunk;   // coefficients per chunk
+constexpr int RSW = kProjWideStride; // smem / chunk-major row stride (double2): 64 B mod 128 B
+constexpr int NWW = 9;               // consumer warps (3 x 3)
+constexpr int WST = 2;               // pipeline stages
+constexpr int kWCoefStage = (WR + WMO) * RSW;    // double2: X rows, then the Phi block
+constexpr int kWApplyStage = WMO * RSW;          // double2: the Phi block
+constexpr int kWCs = WMO + 4;                    // C tile smem stride (4 mod 8: conflict-free)
+constexpr size_t kWCoefSmem = (size_t)WST * kWCoefStage * 16 + 64;
+constexpr size_t kWApplySmem = (size_t)WST * kWApplyStage * 16 + (size_t)WR * kWCs * 16 + 64;
+static_assert(kWCoefSmem <= 232448 && kWApplySmem <= 232448, "wide projector smem");
+constexpr int kWThreads = (NWW + 1) * 32;
+
+__device__ __forceinline__ void wdmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void wsync() {   // the NWW consumer warps only
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NWW * 32) : "memory");
+}
+
+__device__ __forceinline__ int wxrow(const ProjArgs& a, const ProjTile& t, int r) {
+  return a.rows ? a.rows[t.row0 + r] : t.row0 + r;
+}
+
+// chunk-major (32-wide) Phi block: orbitals 0 .. nocc-1 of chunk c of block k
+__device__ __forceinline__ const double2* phiw_at(const ProjArgs& a, int k, int nocc, int c) {
+  return a.phiw + a.phiw_off[k] + (size_t)c * nocc * RSW;
+}
+
+// balanced split of n fragments over 3 warps: [lo, hi) of part p
+__device__ __forceinline__ void split3(int n, int p, int& lo, int& hi) {
+  lo = (p * n) / 3;
+  hi = ((p + 1) * n) / 3;
+}
+
+struct WRange {
+  int u0, u1, nch;   // this CTA's units [u0, u1); chunks per tile
+};
+
+__device__ __forceinline__ WRange wrange(const ProjArgs& a, int nt_host) {
+  const int ntiles = a.ntiles ? *a.ntiles : nt_host;
+  WRange r;
+  r.nch = a.nbp / KW;
+  const long long units = (long long)ntiles * r.nch;
+  const long long per = (units + gridDim.x - 1) / gridDim.x;
+  r.u0 = (int)min(units, per * blockIdx.x);
+  r.u1 = (int)min(units, per * (blockIdx.x + 1));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __maxnreg__(200)
+    k_projw_coef(ProjArgs a, const double2* __restrict__ X, int nt_host,
+                 double2* __restrict__ part, double2* __restrict__ C,
+                 unsigned* __restrict__ counters) {
+  pdl_wait();
+  extern __shared__ __align__(128) double2 sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + WST * kWCoefStage);
+  uint64_t* empty = full + WST;
+  __shared__ bool last;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const WRange R = wrange(a, nt_host);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < WST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (R.u0 >= R.u1) return;
+  if (w == NWW) {   // producer: one Phi block copy + one copy per X row, per unit
+    const double2* xsrc = nullptr;
+    int cur = -1, nocc = 0, nrows = 0, k = 0;
+    for (int u = R.u0, n = 0; u < R.u1; ++u, ++n) {
+      const int s = n % WST;
+      if (n >= WST) mbar_wait(&empty[s], ((n / WST) + 1) & 1);
+      const int tile = u / R.nch, c = u - tile * R.nch;
+      if (tile != cur) {
+        cur = tile;
+        const ProjTile t = a.tiles[tile];
+        k = t.k;
+        nocc = a.nocc[k];
+        nrows = t.nrows;
+        xsrc = nullptr;
+        if (lane < nrows) xsrc = X + (size_t)wxrow(a, t, lane) * a.nbp;
+      }
+      double2* buf = sm + s * kWCoefStage;
+      if (lane == 0) {
+        const uint32_t pb = (uint32_t)nocc * RSW * 16;
+        mbar_expect_tx(&full[s], pb + (uint32_t)nrows * KW * 16);
+        bulk_g2s(buf + WR * RSW, phiw_at(a, k, nocc, c), pb, &full[s]);
+      }
+      __syncwarp();
+      // rows lane, lane + 32, lane + 64 of the tile
+      for (int r = lane; r < nrows; r += 32) {
+        const double2* src = (r == lane) ? xsrc
+                                         : X + (size_t)wxrow(a, a.tiles[tile], r) * a.nbp;
+        bulk_g2s(buf + r * RSW, src + (size_t)c * KW, KW * 16, &full[s]);
+      }
+    }
+    return;
+  }
+  const int r4 = lane >> 2, c4 = lane & 3;
+  const int wm = w / 3, wn = w - 3 * (w / 3);
+  double t1[4][3][2], t2[4][3][2], t3[4][3][2];
+  int seq = 0;
+  for (int u = R.u0; u < R.u1;) {
+    const int tile = u / R.nch;
+    const int uend = min(R.u1, (tile + 1) * R.nch);   // this CTA's run on the tile
+    const ProjTile t = a.tiles[tile];
+    const int nm = a.nocc[t.k];
+    int m_lo, m_hi, n_lo, n_hi;
+    split3((nm + 7) >> 3, wm, m_lo, m_hi);
+    split3((t.nrows + 7) >> 3, wn, n_lo, n_hi);
+    const int cm = m_hi - m_lo, cn = n_hi - n_lo;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        t1[i][j][0] = t1[i][j][1] = 0.0;
+        t2[i][j][0] = t2[i][j][1] = 0.0;
+        t3[i][j][0] = t3[i][j][1] = 0.0;
+      }
+    for (; u < uend; ++u, ++seq) {
+      const int s = seq % WST;
+      mbar_wait(&full[s], (seq / WST) & 1);
+      const double2* xs = sm + s * kWCoefStage;
+      const double2* ps = xs + WR * RSW;
+#pragma unroll 2
+      for (int kk = 0; kk < KW / 4; ++kk) {
+        const int gl = 4 * kk + c4;
+        double2 bv[3];
+        double bs[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          bv[j] = j < cn ? xs[(8 * (n_lo + j) + r4) * RSW + gl] : make_double2(0.0, 0.0);
+          bs[j] = bv[j].x + bv[j].y;
+        }
+        // conj(phi) x: re = pr xr + pi xi, im = pr xi - pi xr (3 real products)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i >= cm) break;
+          const double2 av = ps[(8 * (m_lo + i) + r4) * RSW + gl];
+          const double ad = av.x - av.y;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            if (j >= cn) break;
+            wdmma(t1[i][j][0], t1[i][j][1], av.x, bv[j].x);
+            wdmma(t2[i][j][0], t2[i][j][1], av.y, bv[j].y);
+            wdmma(t3[i][j][0], t3[i][j][1], ad, bs[j]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // ---- flush the run on `tile`: final C, or a partial + fixed-order reduction
+    const int ntiles = a.ntiles ? *a.ntiles : nt_host;
+    const long long units = (long long)ntiles * R.nch;
+    const long long pe = (units + gridDim.x - 1) / gridDim.x;
+    const int first = (int)(((long long)tile * R.nch) / pe);
+    const int lastc = (int)(((long long)(tile + 1) * R.nch - 1) / pe);
+    const int nseg = lastc - first + 1;
+    const int E = t.nrows * nm;                      // valid entries (r, m) -> r * nm + m
+    double2* dst = nseg == 1 ? nullptr : part + (size_t)(tile + blockIdx.x) * (WR * WMO);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i >= cm) break;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (j >= cn) break;
+        const int m = 8 * (m_lo + i) + r4;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = 8 * (n_lo + j) + 2 * c4 + h;
+          if (m < nm && r < t.nrows) {
+            const double2 v = make_double2(t1[i][j][h] + t2[i][j][h],
+                                           t3[i][j][h] - t1[i][j][h] + t2[i][j][h]);
+            if (dst)
+              dst[r * nm + m] = v;
+            else
+              C[(size_t)(t.row0 + r) * a.ldc + m] = v;
+          }
+        }
+      }
+    }
+    if (nseg > 1) {
+      __threadfence();
+      wsync();
+      if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&counters[tile], 1u);
+        last = (prev == (unsigned)nseg - 1);
+      }
+      wsync();
+      if (last) {
+        __threadfence();
+        const double2* p0 = part + (size_t)(tile + first) * (WR * WMO);
+        for (int e = threadIdx.x; e < E; e += NWW * 32) {
+          double2 v = make_double2(0.0, 0.0);
+          for (int q = 0; q < nseg; q += 4) {   // four slot loads in flight, summed in order
+            double2 x4[4];
+#pragma unroll
+            for (int d = 0; d < 4; ++d)
+              x4[d] = q + d < nseg ? __ldcg(&p0[(size_t)(q + d) * (WR * WMO) + e])
+                                   : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) v = cadd(v, x4[d]);
+          }
+          const int r = e / nm, m = e - r * nm;
+          C[(size_t)(t.row0 + r) * a.ldc + m] = v;
+        }
+        if (threadIdx.x == 0) counters[tile] = 0u;
+      }
+      wsync();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __maxnreg__(200)
+    k_projw_apply(ProjArgs a, const double2* __restrict__ C, const double2* __restrict__ Xin,
+                  double2* __restrict__ Y, double ca, double cb, const int* __restrict__ active,
+                  int band_mod, int nt_host) {
+  pdl_wait();
+  extern __shared__ __align__(128) double2 sm[];
+  double2* cs = sm + WST * kWApplyStage;   // C rows of the current tile [WR][kWCs]
+  uint64_t* full = reinterpret_cast<uint64_t*>(cs + WR * kWCs);
+  uint64_t* empty = full + WST;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const WRange R = wrange(a, nt_host);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < WST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (R.u0 >= R.u1) return;
+  if (w == NWW) {
+    for (int u = R.u0, n = 0; u < R.u1; ++u, ++n) {
+      const int s = n % WST;
+      if (n >= WST) mbar_wait(&empty[s], ((n / WST) + 1) & 1);
+      if (lane == 0) {
+        const int tile = u / R.nch, c = u - tile * R.nch;
+        const int k = a.tiles[tile].k, nocc = a.nocc[k];
+        const uint32_t bytes = (uint32_t)nocc * RSW * 16;
+        mbar_expect_tx(&full[s], bytes);
+        bulk_g2s(sm + s * kWApplyStage, phiw_at(a, k, nocc, c), bytes, &full[s]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  const int r4 = lane >> 2, c4 = lane & 3;
+  const int wr = w / 3, wg = w - 3 * (w / 3);
+  const bool want_x = ca != 0.0;
+  int g_lo, g_hi;
+  split3(KW / 8, wg, g_lo, g_hi);   // 4 g fragments per chunk: 1, 1, 2
+  const int cg = g_hi - g_lo;
+  int seq = 0;
+  for (int u = R.u0; u < R.u1;) {
+    const int tile = u / R.nch;
+    const int uend = min(R.u1, (tile + 1) * R.nch);
+    const ProjTile t = a.tiles[tile];
+    const int nm = a.nocc[t.k];
+    wsync();   // every warp is done with the previous tile's C rows
+    for (int i = threadIdx.x; i < t.nrows * nm; i += NWW * 32) {
+      const int r = i / nm, m = i - r * nm;
+      cs[r * kWCs + m] = __ldg(&C[(size_t)(t.row0 + r) * a.ldc + m]);
+    }
+    int r_lo, r_hi;
+    split3((t.nrows + 7) >> 3, wr, r_lo, r_hi);
+    const int cr = r_hi - r_lo;
+    int orow[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int r = 8 * (r_lo + i) + r4;
+      orow[i] = (i < cr && r < t.nrows) ? wxrow(a, t, r) : -1;
+      if (orow[i] >= 0 && active && !active[orow[i] % band_mod]) orow[i] = -1;
+    }
+    wsync();
+    for (; u < uend; ++u, ++seq) {
+      const size_t g0 = (size_t)(u - tile * R.nch) * KW;
+      double2 xv[3][2][2];   // epilogue X values, loaded while the DMMAs run
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            xv[i][j][h] = (want_x && orow[i] >= 0 && j < cg)
+                              ? __ldg(&Xin[(size_t)orow[i] * a.nbp + g0 + 8 * (g_lo + j) +
+                                           2 * c4 + h])
+                              : make_double2(0.0, 0.0);
+      double t1[3][2][2], t2[3][2][2], t3[3][2][2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          t1[i][j][0] = t1[i][j][1] = 0.0;
+          t2[i][j][0] = t2[i][j][1] = 0.0;
+          t3[i][j][0] = t3[i][j][1] = 0.0;
+        }
+      const int s = seq % WST;
+      mbar_wait(&full[s], (seq / WST) & 1);
+      const double2* ps = sm + s * kWApplyStage;
+#pragma unroll 2
+      for (int ms = 0; ms < nm; ms += 4) {
+        const int m = ms + c4;
+        const bool mok = m < nm;   // contraction padding must be exactly zero
+        double2 av[3], bv[2];
+        double as[3], bs[2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {   // A[row j = r4][k = c4] = C[row][m]
+          av[i] = (mok && i < cr) ? cs[(8 * (r_lo + i) + r4) * kWCs + m] : make_double2(0.0, 0.0);
+          as[i] = av[i].x + av[i].y;
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {   // B[k = c4][n = r4] = Phi[m][g]
+          bv[j] = (mok && j < cg) ? ps[m * RSW + 8 * (g_lo + j) + r4] : make_double2(0.0, 0.0);
+          bs[j] = bv[j].x + bv[j].y;
+        }
+        // c phi: re = cr pr - ci pi, im = cr pi + ci pr (3 real products)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          if (i >= cr) break;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (j >= cg) break;
+            wdmma(t1[i][j][0], t1[i][j][1], av[i].x, bv[j].x);
+            wdmma(t2[i][j][0], t2[i][j][1], av[i].y, bv[j].y);
+            wdmma(t3[i][j][0], t3[i][j][1], as[i], bs[j]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int row = orow[i];
+        if (row < 0) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j >= cg) break;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double dr = t1[i][j][h] - t2[i][j][h];
+            const double di = t3[i][j][h] - t1[i][j][h] - t2[i][j][h];
+            Y[(size_t)row * a.nbp + g0 + 8 * (g_lo + j) + 2 * c4 + h] =
+                make_double2(ca * xv[i][j][h].x + cb * dr, ca * xv[i][j][h].y + cb * di);
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+static int projw_configure() {
+  static bool done = false;
+  if (done) return PWB_OK;
+  PWB_CUDA(cudaFuncSetAttribute(k_projw_coef, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kWCoefSmem));
+  PWB_CUDA(cudaFuncSetAttribute(k_projw_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kWApplySmem));
+  done = true;
+  return PWB_OK;
+}
+
+bool projw_enabled() {
+  static const bool off = getenv("PWB_NO_WIDE_PROJ") != nullptr;   // A/B measurement
+  return !off;
+}
+
+int projw_tiles(const std::vector<int>& row_k, std::vector<ProjTile>& out) {
+  out.clear();
+  const int n = (int)row_k.size();
+  for (int i = 0; i < n;) {
+    int j = i;
+    while (j < n && row_k[j] == row_k[i] && j - i < WR) ++j;
+    out.push_back(ProjTile{i, j - i, row_k[i]});
+    i = j;
+  }
+  return (int)out.size();
+}
+
+size_t projw_part_elems(int max_tiles) { return (size_t)(max_tiles + kSM) * WR * WMO; }
+
+int projw_coeffs(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* X,
+                 double2* part, double2* C, unsigned* counters, cudaStream_t st) {
+  if (cap == 0) return PWB_OK;
+  PWB_TRY(projw_configure());
+  a.tiles = dtiles;
+  const long long units = (long long)cap * (a.nbp / KW);
+  const int grid = (int)std::min<long long>(units, kSM);
+  (void)launch_k(k_projw_coef, grid, kWThreads, kWCoefSmem, st, a, X, nt_host, part, C,
+                 counters);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int projw_apply(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* C,
+                const double2* Xin, double2* Y, double ca, double cb, const int* active,
+                int band_mod, cudaStream_t st) {
+  if (cap == 0) return PWB_OK;
+  PWB_TRY(projw_configure());
+  a.tiles = dtiles;
+  const long long units = (long long)cap * (a.nbp / KW);
+  const int grid = (int)std::min<long long>(units, kSM);
+  (void)launch_k(k_projw_apply, grid, kWThreads, kWApplySmem, st, a, C, Xin, Y, ca, cb, active,
+                 band_mod > 0 ? band_mod : 1, nt_host);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+// 32-wide chunk-major copy of the orbital rows (one CTA per (orbital row, chunk))
+__global__ void k_phiw_chunk(const double2* __restrict__ phi, int nbp, int nk,
+                             const int* __restrict__ off, const int* __restrict__ nocc,
+                             const int* __restrict__ phiw_off, double2* __restrict__ phiw) {
+  pdl_wait();
+  const int b = blockIdx.x, c = blockIdx.y;
+  int k = 0;
+  while (k + 1 < nk && off[k + 1] <= b) ++k;
+  const int m = b - off[k];
+  double2* dst = phiw + phiw_off[k] + ((size_t)c * nocc[k] + m) * RSW;
+  for (int i = threadIdx.x; i < RSW; i += blockDim.x)
+    dst[i] = i < KW ? phi[(size_t)b * nbp + (size_t)c * KW + i] : make_double2(0.0, 0.0);
+}
+
+int projw_chunked(const double2* phi, int nbp, const std::vector<int>& off_host,
+                  const std::vector<int>& nocc_host, DevBuf& phiw, DevBuf& d_meta,
+                  cudaStream_t st) {
+  if (nbp % KW) return fail(PWB_ERR_UNSUPPORTED, "wide projector: row stride not a multiple of 32");
+  const int nk = (int)nocc_host.size(), nchunk = nbp / KW;
+  std::vector<int> meta(3 * nk);
+  long long tot = 0;
+  int nband = 0;
+  for (int k = 0; k < nk; ++k) {
+    meta[k] = off_host[k];
+    meta[nk + k] = nocc_host[k];
+    meta[2 * nk + k] = (int)tot;
+    tot += (long long)nchunk * nocc_host[k] * RSW;
+    nband += nocc_host[k];
+  }
+  if (tot > 0x7fffffffLL) return fail(PWB_ERR_UNSUPPORTED, "chunk-major orbitals exceed 2^31");
+  PWB_TRY(phiw.ensure((size_t)std::max<long long>(tot, 1) * sizeof(double2)));
+  PWB_TRY(d_meta.ensure(3 * (size_t)nk * sizeof(int)));
+  PWB_CUDA(cudaMemcpyAsync(d_meta.ptr, meta.data(), meta.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, st));
+  const int* dm = as<int>(d_meta);
+  if (nband > 0) {
+    (void)launch_k(k_phiw_chunk, dim3(nband, nchunk), 64, 0, st, phi, nbp, nk, dm, dm + nk,
+                   dm + 2 * nk, as<double2>(phiw));
+    PWB_LAUNCH_CHECK();
+  }
+  PWB_CUDA(cudaStreamSynchronize(st));   // meta is a host temporary
+  return PWB_OK;
+}
+
+}  // namespace pwb

@@ -207,6 +207,10 @@ int pwb_state_create(pwb_grid* g, const int* nocc_per_k, const double* kweight,
   PWB_CUDA(cudaMemcpy(st->d_band_k.ptr, st->band_k.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
   PWB_TRY(proj_chunked(as<double2>(st->phi), g->nbp, st->off, st->nocc, st->phic, st->phic_meta,
                        nullptr));
+  st->wide_ok = ldc <= kProjWideOcc && g->nbp % kProjWideChunk == 0;
+  if (st->wide_ok)
+    PWB_TRY(projw_chunked(as<double2>(st->phi), g->nbp, st->off, st->nocc, st->phiw,
+                          st->phiw_meta, nullptr));
 
   // per-band coefficients [w*2f/sqrt(Omega), w*f', f', w]
   std::vector<double> coef(4 * (size_t)nb);
@@ -274,7 +278,9 @@ int pwb_project_out(pwb_state* st, int k, int ncol, double* x) {
     PWB_TRY(proj_plan(st->user_plan, key, st->nocc, st->g->nbp));
     st->user_plan_key = key;
   }
-  PWB_TRY(st->user_part.ensure(proj_part_elems(st->user_plan) * sizeof(double2)));
+  size_t pe = proj_part_elems(st->user_plan);
+  if (st->wide_ok) pe = std::max(pe, projw_part_elems((int)st->user_plan.wtiles.size()));
+  PWB_TRY(st->user_part.ensure(pe * sizeof(double2)));
   PWB_TRY(st->user_cmat.ensure((size_t)ncol * st->ldc * sizeof(double2)));
   return project_rows(st, st->user_plan, reinterpret_cast<double2*>(x), nullptr, ncol, nullptr,
                       as<double2>(st->user_part), as<double2>(st->user_cmat), st->g->stream);
@@ -337,7 +343,7 @@ int pwb_chi0_begin(pwb_state* st, int b0, int b1, const double* dv, double* fsum
   // M^T = (Phi^H dvpsi)^T  (response.py:129)
   ProjArgs a = proj_args(st);
   CgBatch& cg = st->cg;
-  PWB_TRY(proj_coeffs(cg.plan1, a, dvpsi, as<double2>(cg.part), as<double2>(st->cm), s));
+  PWB_TRY(proj_coeffs_any(st, cg.plan1, a, dvpsi, as<double2>(cg.part), as<double2>(st->cm), s));
   double* deps = as<double>(st->scal);
   (void)launch_k(k_chi0_eps, 1, 256, 0, s, b0, n, st->ldc, as<int>(st->d_band_k), as<int>(st->d_off),
                                as<double2>(st->cm), as<double>(st->d_coef), deps, fsum);
@@ -367,11 +373,11 @@ static int chi0_finish_impl(pwb_state* st, const double* fsum, double den, doubl
                               c1);
   PWB_LAUNCH_CHECK();
   // delta phi^P = Phi (W o M)  (response.py:138)
-  PWB_TRY(proj_apply(cg.plan1, a, as<double2>(st->cw), nullptr, as<double2>(st->dphi), 0.0, 1.0,
-                     nullptr, n, s));
+  PWB_TRY(proj_apply_any(st, cg.plan1, a, as<double2>(st->cw), nullptr, as<double2>(st->dphi),
+                         0.0, 1.0, nullptr, n, s));
   // rhs = -Q dvpsi (response.py:141), reusing Phi^H dvpsi
-  PWB_TRY(proj_apply(cg.plan1, a, as<double2>(st->cm), as<double2>(st->dvpsi),
-                     as<double2>(cg.rhs), -1.0, 1.0, nullptr, n, s));
+  PWB_TRY(proj_apply_any(st, cg.plan1, a, as<double2>(st->cm), as<double2>(st->dvpsi),
+                         as<double2>(cg.rhs), -1.0, 1.0, nullptr, n, s));
   std::vector<double> tol(tol_host, tol_host + n);
   // results are read back with the accumulation already queued behind the CG loop
   PWB_TRY(cg_solve(st, cg, tol, -1, nullptr, nullptr, true));

@@ -30,7 +30,12 @@ struct IterCtl {
   int* rows2;      // [2n]  rows then rows + n (stacked (x; r) buffer)
   ProjTile* ta;    // tiles over rows
   ProjTile* tb;    // tiles over rows2
+  ProjTile* wa;    // wide tiles (projw.cu) over rows, or null
+  ProjTile* wb;    // wide tiles over rows2
 };
+// ints of IterCtl::hdr: [0] na, [1] tiles A, [2] tiles B, [3] rows still iterating,
+// [4] failure flag, [5] loop count, [6] loop cap, [8] wide tiles A, [9] wide tiles B
+constexpr int kHdrInts = 16;
 
 struct CgBatch {
   int nrows = 0;
@@ -66,7 +71,15 @@ constexpr int kMaxK = 128;  // k blocks handled by the device-side compaction
 ProjArgs proj_args(pwb_state* st);
 int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* active, int band_mod,
                  const int* rows, double2* part, double2* cmat, cudaStream_t s,
-                 const int* ntiles = nullptr, int mult = 1);
+                 const int* ntiles = nullptr, int mult = 1, const int* wntiles = nullptr);
+// C = Phi^H X / Y = ca X + cb Phi C through the wide-tile kernels when the state
+// and plan allow them (device tile counts: a.ntiles for 16-row tiles, wntiles for
+// wide ones), else the 16-row kernels of proj.cu
+int proj_coeffs_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* X,
+                    double2* part, double2* C, cudaStream_t s, const int* wntiles = nullptr);
+int proj_apply_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* C,
+                   const double2* Xin, double2* Y, double ca, double cb, const int* active,
+                   int band_mod, cudaStream_t s, const int* wntiles = nullptr);
 int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands);
 // defer: enqueue the result readback and return without synchronising; the
 // caller synchronises the stream (after queueing more work) and calls cg_check
@@ -92,6 +105,8 @@ struct pwb_state {
   pwb::DevBuf phi, d_off, d_nocc, d_band_k, d_eps, d_pshift, d_coef, vloc, rho, wt;
   pwb::DevBuf vloct;         // x-major V_local for the fused pencil multiply
   pwb::DevBuf phic, phic_meta;   // chunk-major orbitals for the projector (proj.cuh)
+  pwb::DevBuf phiw, phiw_meta;   // 32-wide chunk-major orbitals (wide tiles, projw.cu)
+  bool wide_ok = false;          // every k block has <= kProjWideOcc orbitals
   pwb::DevBuf psir;          // psi(r) cache for rows [shard_b0, shard_b1)
   int psir_b0 = -1, psir_b1 = -1;
   // chi0 workspaces

@@ -3,6 +3,7 @@
 // (fixed grid, fixed order), so every scalar is bitwise reproducible; the
 // MGS step keeps the Hessenberg entries on the device and returns the
 // column to the host once per Arnoldi step.
+#include <algorithm>
 #include <cmath>
 
 #include "grid.cuh"
@@ -59,6 +60,26 @@ __global__ void k_axpy_dev(int n, const double* __restrict__ c, const double* __
 __global__ void k_axpy_host(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
   pdl_wait();
   for (int i = blockIdx.x * NTV + threadIdx.x; i < n; i += gridDim.x * NTV) y[i] += a * x[i];
+}
+
+// out = a x + b y (y == NULL: a x), each product and the sum rounded separately
+// (no FMA contraction) so the result equals numpy's `a * x + b * y`
+__global__ void k_axpby(long long n, double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ out) {
+  pdl_wait();
+  for (long long i = blockIdx.x * (long long)NTV + threadIdx.x; i < n;
+       i += (long long)gridDim.x * NTV) {
+    const double ax = __dmul_rn(a, x[i]);
+    out[i] = y ? __dadd_rn(ax, __dmul_rn(b, y[i])) : ax;
+  }
+}
+
+// out = x / d (IEEE division, numpy's `x / d`)
+__global__ void k_div(long long n, const double* __restrict__ x, double d, double* __restrict__ out) {
+  pdl_wait();
+  for (long long i = blockIdx.x * (long long)NTV + threadIdx.x; i < n;
+       i += (long long)gridDim.x * NTV)
+    out[i] = __ddiv_rn(x[i], d);
 }
 
 // v = w / h (or 0 when h == 0: lucky breakdown, igmres.py:99-102)
@@ -193,6 +214,25 @@ extern "C" {
 
 int pwb_vec_dot(pwb_grid* g, int n, const double* x, const double* y, double* out_dev) {
   return dot_into(vctx(g), n, x, y, out_dev, 0, 0);
+}
+
+int pwb_vec_axpby(pwb_grid* g, long long n, double a, const double* x, double b, const double* y,
+                  double* out) {
+  if (n <= 0) return PWB_OK;
+  if (!x || !out) return fail(PWB_ERR_VALUE, "null vector");
+  const int nb = (int)std::min<long long>(4LL * kSM, (n + NTV - 1) / NTV);
+  (void)launch_k(k_axpby, nb, NTV, 0, vctx(g).stream, n, a, x, b, y, out);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
+}
+
+int pwb_vec_div(pwb_grid* g, long long n, const double* x, double d, double* out) {
+  if (n <= 0) return PWB_OK;
+  if (!x || !out) return fail(PWB_ERR_VALUE, "null vector");
+  const int nb = (int)std::min<long long>(4LL * kSM, (n + NTV - 1) / NTV);
+  (void)launch_k(k_div, nb, NTV, 0, vctx(g).stream, n, x, d, out);
+  PWB_LAUNCH_CHECK();
+  return PWB_OK;
 }
 
 int pwb_vec_axpy(pwb_grid* g, int n, double a, const double* x, double* y) {

@@ -24,6 +24,7 @@ from .errors import NonConvergenceError
 from .groundstate import ham_counter
 from .igmres import igmres_solve
 from .kernels import KernelSpec, KerkerSpec, apply_kerker_dev
+from .ops import axpby_dev, div_dev
 from .response import _norm, apply_chi0_dev, apply_dielectric_dev, orbital_row_norm
 from .strategies import StrategySpec, parse_strategy, tolerances_k
 
@@ -76,19 +77,21 @@ def build_rhs(gs, dv0_t, spec, rows=None):
         return torch.zeros_like(dv0_t), 0, None
     if rows is None:
         rows = row_norms(gs) if spec.kind == "grt" else [np.nan] * len(blocks)
+    h = ds.grid.handle
+    unit = div_dev(h, dv0_t, nrm)
     if spec.kind == "d10n":
         prov = tolerances_k(blocks, StrategySpec("d10", spec.preconditioned, spec.tau, spec.m),
                             0, rows, kv_norm=nrm, rhs_norm=1.0)
-        d0, st0 = apply_chi0_dev(gs, dv0_t / nrm, prov)
+        d0, st0 = apply_chi0_dev(gs, unit, prov)
         rn = _norm(ds.grid, d0) * nrm
         tols = tolerances_k(blocks, spec, 0, rows, kv_norm=nrm, rhs_norm=rn)
         if np.all(tols >= prov):
-            return nrm * d0, st0.ham_applications, prov
-        d0, st = apply_chi0_dev(gs, dv0_t / nrm, tols)
-        return nrm * d0, st0.ham_applications + st.ham_applications, tols
+            return axpby_dev(h, nrm, d0), st0.ham_applications, prov
+        d0, st = apply_chi0_dev(gs, unit, tols)
+        return axpby_dev(h, nrm, d0), st0.ham_applications + st.ham_applications, tols
     tols = tolerances_k(blocks, spec, 0, rows, kv_norm=nrm, rhs_norm=1.0)
-    d0, st = apply_chi0_dev(gs, dv0_t / nrm, tols)
-    return nrm * d0, st.ham_applications, tols
+    d0, st = apply_chi0_dev(gs, unit, tols)
+    return axpby_dev(h, nrm, d0), st.ham_applications, tols
 
 
 def true_residual(gs, kernel, x_t, b_t):
@@ -96,7 +99,8 @@ def true_residual(gs, kernel, x_t, b_t):
     blocks, _ = state_blocks(gs)
     n = sum(b.n_occ for b in blocks)
     out, _, _ = apply_dielectric_dev(gs, kernel, x_t, np.full(n, TIGHT_CG_TOL))
-    return _norm(device_state(gs).grid, b_t - out)
+    dg = device_state(gs).grid
+    return _norm(dg, axpby_dev(dg.handle, 1.0, b_t, -1.0, out))
 
 
 def solve_dyson(gs, dv0, strategy="bal", tau=1e-8, m=10, xc=None, kerker_alpha=0.8,

@@ -137,3 +137,21 @@ def kerker_apply_dev(dg, alpha, v_t):
     _lib.check(_lib.load().pwb_kerker_apply(dg.handle, float(alpha), ptr(v_t), ptr(out)),
                "kerker_apply")
     return out
+
+
+def axpby_dev(handle, a, x_t, b=0.0, y_t=None, out=None):
+    """a x + b y (numpy's rounding: no FMA contraction) on float64 device vectors."""
+    torch = torch_mod()
+    out = torch.empty_like(x_t) if out is None else out
+    _lib.check(_lib.load().pwb_vec_axpby(handle, x_t.numel(), float(a), ptr(x_t), float(b),
+                                         ptr(y_t), ptr(out)), "vec_axpby")
+    return out
+
+
+def div_dev(handle, x_t, d, out=None):
+    """x / d on a float64 device vector."""
+    torch = torch_mod()
+    out = torch.empty_like(x_t) if out is None else out
+    _lib.check(_lib.load().pwb_vec_div(handle, x_t.numel(), ptr(x_t), float(d), ptr(out)),
+               "vec_div")
+    return out

@@ -26,6 +26,7 @@ from . import _lib
 from .device import device_grid, device_state, ptr, state_blocks, torch_mod
 from .groundstate import ham_counter
 from .kernels import KernelSpec, apply_kernel_dev
+from .ops import axpby_dev, div_dev
 
 DEGENERACY_RTOL = 1e-8
 IMAG_EIGENSHIFT_RTOL = 1e-10
@@ -152,16 +153,17 @@ def apply_dielectric_dev(gs, kernel, v_t, tolerances):
     kv = _norm(ds.grid, u)
     if kv == 0.0:
         return v_t.clone(), 0.0, None
+    h = ds.grid.handle
     if callable(tolerances):
         # the tolerance vector depends on |Kv| only: build chi0's right-hand side on
         # the GPU while the host evaluates the strategy (strategies.py, numpy)
-        ds.chi0_begin(u / kv)
+        ds.chi0_begin(div_dev(h, u, kv))
         tols = _validate(gs, tolerances(kv))
         drho, its = ds.chi0_finish(tols)
         stats = _stats(its, tols)
     else:
-        drho, stats = apply_chi0_dev(gs, u / kv, tolerances)
-    return v_t - kv * drho, kv, stats
+        drho, stats = apply_chi0_dev(gs, div_dev(h, u, kv), tolerances)
+    return axpby_dev(h, 1.0, v_t, -kv, drho), kv, stats
 
 
 def _norm(dg, x):

@@ -17,6 +17,8 @@ def main():
     p.add_argument("--seed", type=int, default=None)
     p.add_argument("--tol", type=float, default=1e-9)
     p.add_argument("--scan", type=int, default=0, help="scan seeds 0..N-1 at loose tol")
+    p.add_argument("--n-electrons", type=int, nargs="*", default=None,
+                   help="run the SCF for each of these electron counts (config 2 calibration)")
     args = p.parse_args()
     if args.scan:
         return scan(args)
@@ -29,6 +31,28 @@ def main():
     model = spec["model"]
     if args.temperature is not None:
         model = replace(model, temperature=args.temperature)
+    if args.n_electrons:
+        from paper_2505_02319_b200.groundstate import fermi_and_occupations, smearing_function
+        for nel in args.n_electrons:
+            m = replace(model, n_electrons=nel)
+            t0 = time.perf_counter()
+            try:
+                gs = run_scf_gpu(m, kgrid=spec["params"]["kgrid"], tol=args.tol, verbose=False,
+                                 n_states=nel // 2 + max(6, nel // 4) + 20)
+            except Exception as err:  # noqa: BLE001
+                print(f"n_el {nel}: {err}", flush=True)
+                continue
+            e = np.asarray(gs.eps_all).reshape(-1)
+            # N_occ implied by this spectrum for neighbouring electron counts
+            occf, _ = smearing_function(m.smearing)
+            implied = {}
+            for n2 in range(nel - 16, nel + 17, 2):
+                mu, _ = fermi_and_occupations(e, n2, m.temperature, m.smearing)
+                f = occf((e - mu) / m.temperature)
+                implied[n2] = int(np.max(np.nonzero(f > m.occupation_threshold)[0])) + 1
+            print(f"n_el {nel}: n_occ {gs.n_occ} (scf {time.perf_counter() - t0:.0f} s, "
+                  f"mu {gs.fermi_level:.5f}); same spectrum implies {implied}", flush=True)
+        return
     t0 = time.perf_counter()
     gs = run_scf_gpu(model, kgrid=spec["params"]["kgrid"], tol=args.tol, verbose=True)
     dt = time.perf_counter() - t0
