@@ -72,7 +72,14 @@ def build_workload(cfg):
     """(gs, dv0 numpy, params) for a BASELINE config, seeded: the ground
     state from the GPU SCF (setup, not timed), dV0 drawn from the same generator
     after the wells (paper_2505_02319_b200.cli.make_workload)."""
-    from paper_2505_02319_b200.cli import make_workload
+    from paper_2505_02319_b200.cli import make_workload, read_workload
+    wl = os.environ.get("PWB_WORKLOAD")   # development: reuse a `cli ground-state` directory
+    if wl and os.path.exists(os.path.join(wl, "workload.json")):
+        gs, dv0, params = read_workload(wl)
+        if params.get("config") != cfg:
+            raise SystemExit(f"PWB_WORKLOAD holds config {params.get('config')}, not {cfg}")
+        params["kgrid"] = tuple(params["kgrid"])
+        return gs, dv0, params
     return make_workload(cfg)
 
 

@@ -260,12 +260,16 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
       t += (kcnt[k] + kProjTileRows - 1) / kProjTileRows;
       wt += (kcnt[k] + kProjWideRows - 1) / kProjWideRows;
     }
+    // one projector path per iteration: the wide-tile kernels when the live rows
+    // fill the wide tiles (>= wide_min rows per tile on average), else the
+    // 16-row kernels; the other pair is launched too and exits on its zero count
+    const bool wide = ctl.wa != nullptr && wt > 0 && na >= ctl.wide_min * wt;
     ctl.hdr[0] = na;
-    ctl.hdr[1] = t;
-    ctl.hdr[2] = 2 * t;
+    ctl.hdr[1] = wide ? 0 : t;
+    ctl.hdr[2] = wide ? 0 : 2 * t;
     ctl.hdr[3] = 0;   // rows still iterating after this iteration (k_cg_resid counts)
-    ctl.hdr[8] = wt;  // wide tiles over rows / over the stacked rows
-    ctl.hdr[9] = 2 * wt;
+    ctl.hdr[8] = wide ? wt : 0;  // wide tiles over rows / over the stacked rows
+    ctl.hdr[9] = wide ? 2 * wt : 0;
     carry = t;
     wcarry = wt;
   }
@@ -330,32 +334,42 @@ ProjArgs proj_args(pwb_state* st) {
   return a;
 }
 
+int projw_min_rows() {
+  static const int v = getenv("PWB_WIDE_MIN_ROWS") ? atoi(getenv("PWB_WIDE_MIN_ROWS")) : 32;
+  return v;
+}
+
+// host plans: wide when the rows fill the wide tiles; device plans: the choice is
+// made per call by k_compact through the tile counts (both paths are launched)
 static bool use_wide(const pwb_state* st, const ProjPlan& pl, const int* ntiles,
                      const int* wntiles) {
-  return st->wide_ok && projw_enabled() && plan_wide_tiles(pl) > 0 &&
-         (ntiles == nullptr) == (wntiles == nullptr);
+  if (!st->wide_ok || !projw_enabled() || plan_wide_tiles(pl) == 0) return false;
+  if ((ntiles == nullptr) != (wntiles == nullptr)) return false;
+  if (ntiles) return true;
+  return pl.nrows >= projw_min_rows() * (int)pl.wtiles.size();
 }
 
 int proj_coeffs_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* X,
                     double2* part, double2* C, cudaStream_t s, const int* wntiles) {
-  if (use_wide(st, pl, a.ntiles, wntiles)) {
-    a.ntiles = wntiles;
-    return projw_coeffs(reinterpret_cast<const ProjTile*>(pl.dwtiles.ptr), (int)pl.wtiles.size(),
-                        plan_wide_tiles(pl), a, X, part, C,
-                        reinterpret_cast<unsigned*>(pl.wcounters.ptr), s);
-  }
-  return proj_coeffs(pl, a, X, part, C, s);
+  if (!use_wide(st, pl, a.ntiles, wntiles)) return proj_coeffs(pl, a, X, part, C, s);
+  if (a.ntiles) PWB_TRY(proj_coeffs(pl, a, X, part, C, s));   // exits when wide is chosen
+  ProjArgs w = a;
+  w.ntiles = wntiles;
+  return projw_coeffs(reinterpret_cast<const ProjTile*>(pl.dwtiles.ptr), (int)pl.wtiles.size(),
+                      plan_wide_tiles(pl), w, X, part, C,
+                      reinterpret_cast<unsigned*>(pl.wcounters.ptr), s);
 }
 
 int proj_apply_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* C,
                    const double2* Xin, double2* Y, double ca, double cb, const int* active,
                    int band_mod, cudaStream_t s, const int* wntiles) {
-  if (use_wide(st, pl, a.ntiles, wntiles)) {
-    a.ntiles = wntiles;
-    return projw_apply(reinterpret_cast<const ProjTile*>(pl.dwtiles.ptr), (int)pl.wtiles.size(),
-                       plan_wide_tiles(pl), a, C, Xin, Y, ca, cb, active, band_mod, s);
-  }
-  return proj_apply(pl, a, C, Xin, Y, ca, cb, active, band_mod, s);
+  if (!use_wide(st, pl, a.ntiles, wntiles))
+    return proj_apply(pl, a, C, Xin, Y, ca, cb, active, band_mod, s);
+  if (a.ntiles) PWB_TRY(proj_apply(pl, a, C, Xin, Y, ca, cb, active, band_mod, s));
+  ProjArgs w = a;
+  w.ntiles = wntiles;
+  return projw_apply(reinterpret_cast<const ProjTile*>(pl.dwtiles.ptr), (int)pl.wtiles.size(),
+                     plan_wide_tiles(pl), w, C, Xin, Y, ca, cb, active, band_mod, s);
 }
 
 // Q X in place for the rows of a plan (masked by `active` when given)
@@ -457,8 +471,10 @@ int cg_setup(pwb_state* st, CgBatch& cg, const std::vector<int>& bands) {
   cg.ctl.rows2 = cg.ctl.rows + n;
   cg.ctl.ta = reinterpret_cast<ProjTile*>(cg.pa.dtiles.ptr);
   cg.ctl.tb = reinterpret_cast<ProjTile*>(cg.pb.dtiles.ptr);
-  cg.ctl.wa = wcap > 0 ? reinterpret_cast<ProjTile*>(cg.pa.dwtiles.ptr) : nullptr;
-  cg.ctl.wb = wcap > 0 ? reinterpret_cast<ProjTile*>(cg.pb.dwtiles.ptr) : nullptr;
+  cg.ctl.wa = (wcap > 0 && projw_enabled()) ? reinterpret_cast<ProjTile*>(cg.pa.dwtiles.ptr)
+                                             : nullptr;
+  cg.ctl.wb = cg.ctl.wa ? reinterpret_cast<ProjTile*>(cg.pb.dwtiles.ptr) : nullptr;
+  cg.ctl.wide_min = projw_min_rows();
   std::vector<double> eps(n), ps(n);
   for (int i = 0; i < n; ++i) {
     eps[i] = st->eps[bands[i]];

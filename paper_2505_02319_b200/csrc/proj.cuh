@@ -11,9 +11,9 @@ namespace pwb {
 constexpr int kProjTileRows = 16;   // rows per projector tile (<= 2 DMMA n-fragments)
 constexpr int kProjChunk = 64;      // sphere coefficients per pipeline chunk
 constexpr int kProjRowStride = kProjChunk + 4;   // padded smem / chunk-major row (double2)
-// wide tiles (projw.cu): up to 72 rows of one k block against all its <= 80 orbitals
+// wide tiles (projw.cu): up to 72 rows of one k block against all its <= 72 orbitals
 constexpr int kProjWideRows = 72;
-constexpr int kProjWideOcc = 80;
+constexpr int kProjWideOcc = 72;
 constexpr int kProjWideChunk = 32;
 constexpr int kProjWideStride = kProjWideChunk + 4;
 

@@ -1,5 +1,5 @@
 // Wide-tile projector: Q X = X - Phi (Phi^H X) with one tile = up to 72 rows
-// of ONE k block against ALL its orbitals (<= 80), reference
+// of ONE k block against ALL its orbitals (<= 72), reference
 // sternheimer.py:28-30.  This is the shape of a Sternheimer batch at full
 // width (every occupied band of a k point iterates: rows_k = N_occ,k), where
 // the 16-row tiles of proj.cu re-stream Phi_k once per 16 rows and the X rows
@@ -16,12 +16,15 @@
 //           stays in smem across its chunks.
 //
 // Operands arrive by TMA bulk copies (one copy for the chunk's Phi block from
-// the 32-wide chunk-major copy, one 512 B copy per gathered X row) into a
-// 2-stage smem ring driven by a producer warp and full/empty mbarriers.  The
-// nine consumer warps form a 3 x 3 grid over the output fragments (8 x 8
-// DMMA tiles, mma.sync.m8n8k4.f64 -> DMMA.8x8x4), so a warp reuses each
-// loaded A fragment across its n fragments and vice versa; complex products
-// use three real DMMAs (Gauss), as in proj.cu.
+// the 32-wide chunk-major copy, one 512 B copy per gathered X row) into an
+// smem ring with full/empty mbarriers; warp 0 refills a stage once every warp
+// has released it (no separate producer warp).  Twelve compute warps -- three
+// per SM sub-partition, so the four DMMA pipes are loaded evenly (nine warps
+// cap the busiest sub-partition at 3 of 4 warps' worth: 75%) -- form a 4 x 3
+// grid over the output fragments (8 x 8 DMMA tiles, mma.sync.m8n8k4.f64 ->
+// DMMA.8x8x4), so a warp reuses each loaded A fragment across its n
+// fragments and vice versa; complex products use three real DMMAs (Gauss),
+// as in proj.cu.
 #include <cstring>
 
 #include "proj.cuh"
@@ -30,18 +33,19 @@
 namespace pwb {
 
 constexpr int WR = kProjWideRows;    // rows per wide tile (9 n fragments)
-constexpr int WMO = kProjWideOcc;    // orbitals per k block (10 m fragments)
+constexpr int WMO = kProjWideOcc;    // orbitals per k block (9 m fragments)
 constexpr int KW = kProjWideChunk;   // coefficients per chunk
 constexpr int RSW = kProjWideStride; // smem / chunk-major row stride (double2): 64 B mod 128 B
-constexpr int NWW = 9;               // consumer warps (3 x 3)
-constexpr int WST = 2;               // pipeline stages
+constexpr int NWW = 12;              // compute warps (3 per SM sub-partition)
+constexpr int WST = 2;               // coef pipeline stages
+constexpr int WSA = 3;               // apply pipeline stages
 constexpr int kWCoefStage = (WR + WMO) * RSW;    // double2: X rows, then the Phi block
 constexpr int kWApplyStage = WMO * RSW;          // double2: the Phi block
 constexpr int kWCs = WMO + 4;                    // C tile smem stride (4 mod 8: conflict-free)
 constexpr size_t kWCoefSmem = (size_t)WST * kWCoefStage * 16 + 64;
-constexpr size_t kWApplySmem = (size_t)WST * kWApplyStage * 16 + (size_t)WR * kWCs * 16 + 64;
+constexpr size_t kWApplySmem = (size_t)WSA * kWApplyStage * 16 + (size_t)WR * kWCs * 16 + 64;
 static_assert(kWCoefSmem <= 232448 && kWApplySmem <= 232448, "wide projector smem");
-constexpr int kWThreads = (NWW + 1) * 32;
+constexpr int kWThreads = NWW * 32;
 
 __device__ __forceinline__ void wdmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -49,9 +53,6 @@ __device__ __forceinline__ void wdmma(double& d0, double& d1, double a, double b
       : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void wsync() {   // the NWW consumer warps only
-  asm volatile("bar.sync 1, %0;\n" ::"n"(NWW * 32) : "memory");
-}
 
 __device__ __forceinline__ int wxrow(const ProjArgs& a, const ProjTile& t, int r) {
   return a.rows ? a.rows[t.row0 + r] : t.row0 + r;
@@ -62,10 +63,10 @@ __device__ __forceinline__ const double2* phiw_at(const ProjArgs& a, int k, int 
   return a.phiw + a.phiw_off[k] + (size_t)c * nocc * RSW;
 }
 
-// balanced split of n fragments over 3 warps: [lo, hi) of part p
-__device__ __forceinline__ void split3(int n, int p, int& lo, int& hi) {
-  lo = (p * n) / 3;
-  hi = ((p + 1) * n) / 3;
+// balanced split of n fragments over `parts` warps: [lo, hi) of part p
+__device__ __forceinline__ void splitn(int n, int p, int parts, int& lo, int& hi) {
+  lo = (p * n) / parts;
+  hi = ((p + 1) * n) / parts;
 }
 
 struct WRange {
@@ -84,7 +85,7 @@ __device__ __forceinline__ WRange wrange(const ProjArgs& a, int nt_host) {
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(kWThreads, 1)
     k_projw_coef(ProjArgs a, const double2* __restrict__ X, int nt_host,
                  double2* __restrict__ part, double2* __restrict__ C,
                  unsigned* __restrict__ counters) {
@@ -104,41 +105,27 @@ __global__ void __maxnreg__(200)
   }
   __syncthreads();
   if (R.u0 >= R.u1) return;
-  if (w == NWW) {   // producer: one Phi block copy + one copy per X row, per unit
-    const double2* xsrc = nullptr;
-    int cur = -1, nocc = 0, nrows = 0, k = 0;
-    for (int u = R.u0, n = 0; u < R.u1; ++u, ++n) {
-      const int s = n % WST;
-      if (n >= WST) mbar_wait(&empty[s], ((n / WST) + 1) & 1);
-      const int tile = u / R.nch, c = u - tile * R.nch;
-      if (tile != cur) {
-        cur = tile;
-        const ProjTile t = a.tiles[tile];
-        k = t.k;
-        nocc = a.nocc[k];
-        nrows = t.nrows;
-        xsrc = nullptr;
-        if (lane < nrows) xsrc = X + (size_t)wxrow(a, t, lane) * a.nbp;
-      }
-      double2* buf = sm + s * kWCoefStage;
-      if (lane == 0) {
-        const uint32_t pb = (uint32_t)nocc * RSW * 16;
-        mbar_expect_tx(&full[s], pb + (uint32_t)nrows * KW * 16);
-        bulk_g2s(buf + WR * RSW, phiw_at(a, k, nocc, c), pb, &full[s]);
-      }
-      __syncwarp();
-      // rows lane, lane + 32, lane + 64 of the tile
-      for (int r = lane; r < nrows; r += 32) {
-        const double2* src = (r == lane) ? xsrc
-                                         : X + (size_t)wxrow(a, a.tiles[tile], r) * a.nbp;
-        bulk_g2s(buf + r * RSW, src + (size_t)c * KW, KW * 16, &full[s]);
-      }
+  // warp 0 fills stage s with unit u: one Phi block copy + one copy per X row
+  auto fill = [&](int u, int s) {
+    const int tile = u / R.nch, c = u - tile * R.nch;
+    const ProjTile t = a.tiles[tile];
+    const int nocc = a.nocc[t.k];
+    double2* buf = sm + s * kWCoefStage;
+    if (lane == 0) {
+      const uint32_t pb = (uint32_t)nocc * RSW * 16;
+      mbar_expect_tx(&full[s], pb + (uint32_t)t.nrows * KW * 16);
+      bulk_g2s(buf + WR * RSW, phiw_at(a, t.k, nocc, c), pb, &full[s]);
     }
-    return;
-  }
+    __syncwarp();
+    for (int r = lane; r < t.nrows; r += 32)
+      bulk_g2s(buf + r * RSW, X + (size_t)wxrow(a, t, r) * a.nbp + (size_t)c * KW, KW * 16,
+               &full[s]);
+  };
+  if (w == 0)
+    for (int q = 0; q < WST && R.u0 + q < R.u1; ++q) fill(R.u0 + q, q);
   const int r4 = lane >> 2, c4 = lane & 3;
-  const int wm = w / 3, wn = w - 3 * (w / 3);
-  double t1[4][3][2], t2[4][3][2], t3[4][3][2];
+  const int wm = w / 3, wn = w - 3 * (w / 3);   // 4 (m) x 3 (n) warp grid
+  double t1[3][3][2], t2[3][3][2], t3[3][3][2];
   int seq = 0;
   for (int u = R.u0; u < R.u1;) {
     const int tile = u / R.nch;
@@ -146,11 +133,11 @@ __global__ void __maxnreg__(200)
     const ProjTile t = a.tiles[tile];
     const int nm = a.nocc[t.k];
     int m_lo, m_hi, n_lo, n_hi;
-    split3((nm + 7) >> 3, wm, m_lo, m_hi);
-    split3((t.nrows + 7) >> 3, wn, n_lo, n_hi);
+    splitn((nm + 7) >> 3, wm, 4, m_lo, m_hi);
+    splitn((t.nrows + 7) >> 3, wn, 3, n_lo, n_hi);
     const int cm = m_hi - m_lo, cn = n_hi - n_lo;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 3; ++i)
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         t1[i][j][0] = t1[i][j][1] = 0.0;
@@ -174,7 +161,7 @@ __global__ void __maxnreg__(200)
         }
         // conj(phi) x: re = pr xr + pi xi, im = pr xi - pi xr (3 real products)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 3; ++i) {
           if (i >= cm) break;
           const double2 av = ps[(8 * (m_lo + i) + r4) * RSW + gl];
           const double ad = av.x - av.y;
@@ -189,6 +176,10 @@ __global__ void __maxnreg__(200)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (w == 0 && u + WST < R.u1) {   // refill stage s once every warp released it
+        mbar_wait(&empty[s], (seq / WST) & 1);
+        fill(u + WST, s);
+      }
     }
     // ---- flush the run on `tile`: final C, or a partial + fixed-order reduction
     const int ntiles = a.ntiles ? *a.ntiles : nt_host;
@@ -200,7 +191,7 @@ __global__ void __maxnreg__(200)
     const int E = t.nrows * nm;                      // valid entries (r, m) -> r * nm + m
     double2* dst = nseg == 1 ? nullptr : part + (size_t)(tile + blockIdx.x) * (WR * WMO);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 3; ++i) {
       if (i >= cm) break;
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
@@ -222,12 +213,12 @@ __global__ void __maxnreg__(200)
     }
     if (nseg > 1) {
       __threadfence();
-      wsync();
+      __syncthreads();
       if (threadIdx.x == 0) {
         const unsigned prev = atomicAdd(&counters[tile], 1u);
         last = (prev == (unsigned)nseg - 1);
       }
-      wsync();
+      __syncthreads();
       if (last) {
         __threadfence();
         const double2* p0 = part + (size_t)(tile + first) * (WR * WMO);
@@ -247,25 +238,25 @@ __global__ void __maxnreg__(200)
         }
         if (threadIdx.x == 0) counters[tile] = 0u;
       }
-      wsync();
+      __syncthreads();
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(kWThreads, 1)
     k_projw_apply(ProjArgs a, const double2* __restrict__ C, const double2* __restrict__ Xin,
                   double2* __restrict__ Y, double ca, double cb, const int* __restrict__ active,
                   int band_mod, int nt_host) {
   pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
-  double2* cs = sm + WST * kWApplyStage;   // C rows of the current tile [WR][kWCs]
+  double2* cs = sm + WSA * kWApplyStage;   // C rows of the current tile [WR][kWCs]
   uint64_t* full = reinterpret_cast<uint64_t*>(cs + WR * kWCs);
-  uint64_t* empty = full + WST;
+  uint64_t* empty = full + WSA;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const WRange R = wrange(a, nt_host);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < WST; ++s) {
+    for (int s = 0; s < WSA; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWW);
     }
@@ -273,40 +264,31 @@ __global__ void __maxnreg__(200)
   }
   __syncthreads();
   if (R.u0 >= R.u1) return;
-  if (w == NWW) {
-    for (int u = R.u0, n = 0; u < R.u1; ++u, ++n) {
-      const int s = n % WST;
-      if (n >= WST) mbar_wait(&empty[s], ((n / WST) + 1) & 1);
-      if (lane == 0) {
-        const int tile = u / R.nch, c = u - tile * R.nch;
-        const int k = a.tiles[tile].k, nocc = a.nocc[k];
-        const uint32_t bytes = (uint32_t)nocc * RSW * 16;
-        mbar_expect_tx(&full[s], bytes);
-        bulk_g2s(sm + s * kWApplyStage, phiw_at(a, k, nocc, c), bytes, &full[s]);
-      }
-      __syncwarp();
-    }
-    return;
-  }
+  auto fill = [&](int u, int s) {   // warp 0, lane 0: the chunk's Phi block
+    const int tile = u / R.nch, c = u - tile * R.nch;
+    const int k = a.tiles[tile].k, nocc = a.nocc[k];
+    const uint32_t bytes = (uint32_t)nocc * RSW * 16;
+    mbar_expect_tx(&full[s], bytes);
+    bulk_g2s(sm + s * kWApplyStage, phiw_at(a, k, nocc, c), bytes, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int q = 0; q < WSA && R.u0 + q < R.u1; ++q) fill(R.u0 + q, q);
   const int r4 = lane >> 2, c4 = lane & 3;
-  const int wr = w / 3, wg = w - 3 * (w / 3);
+  const int wr = w >> 2, wg = w & 3;   // 3 (row groups) x 4 (g fragments of the chunk)
   const bool want_x = ca != 0.0;
-  int g_lo, g_hi;
-  split3(KW / 8, wg, g_lo, g_hi);   // 4 g fragments per chunk: 1, 1, 2
-  const int cg = g_hi - g_lo;
   int seq = 0;
   for (int u = R.u0; u < R.u1;) {
     const int tile = u / R.nch;
     const int uend = min(R.u1, (tile + 1) * R.nch);
     const ProjTile t = a.tiles[tile];
     const int nm = a.nocc[t.k];
-    wsync();   // every warp is done with the previous tile's C rows
+    __syncthreads();   // every warp is done with the previous tile's C rows
     for (int i = threadIdx.x; i < t.nrows * nm; i += NWW * 32) {
       const int r = i / nm, m = i - r * nm;
       cs[r * kWCs + m] = __ldg(&C[(size_t)(t.row0 + r) * a.ldc + m]);
     }
     int r_lo, r_hi;
-    split3((t.nrows + 7) >> 3, wr, r_lo, r_hi);
+    splitn((t.nrows + 7) >> 3, wr, 3, r_lo, r_hi);
     const int cr = r_hi - r_lo;
     int orow[3];
 #pragma unroll
@@ -315,77 +297,60 @@ __global__ void __maxnreg__(200)
       orow[i] = (i < cr && r < t.nrows) ? wxrow(a, t, r) : -1;
       if (orow[i] >= 0 && active && !active[orow[i] % band_mod]) orow[i] = -1;
     }
-    wsync();
+    __syncthreads();
     for (; u < uend; ++u, ++seq) {
-      const size_t g0 = (size_t)(u - tile * R.nch) * KW;
-      double2 xv[3][2][2];   // epilogue X values, loaded while the DMMAs run
+      const size_t g0 = (size_t)(u - tile * R.nch) * KW + 8 * wg;
+      double2 xv[3][2];   // epilogue X values, loaded while the DMMAs run
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int h = 0; h < 2; ++h)
+          xv[i][h] = (want_x && orow[i] >= 0)
+                         ? __ldg(&Xin[(size_t)orow[i] * a.nbp + g0 + 2 * c4 + h])
+                         : make_double2(0.0, 0.0);
+      double t1[3][2], t2[3][2], t3[3][2];
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            xv[i][j][h] = (want_x && orow[i] >= 0 && j < cg)
-                              ? __ldg(&Xin[(size_t)orow[i] * a.nbp + g0 + 8 * (g_lo + j) +
-                                           2 * c4 + h])
-                              : make_double2(0.0, 0.0);
-      double t1[3][2][2], t2[3][2][2], t3[3][2][2];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          t1[i][j][0] = t1[i][j][1] = 0.0;
-          t2[i][j][0] = t2[i][j][1] = 0.0;
-          t3[i][j][0] = t3[i][j][1] = 0.0;
-        }
-      const int s = seq % WST;
-      mbar_wait(&full[s], (seq / WST) & 1);
-      const double2* ps = sm + s * kWApplyStage;
+      for (int i = 0; i < 3; ++i) {
+        t1[i][0] = t1[i][1] = 0.0;
+        t2[i][0] = t2[i][1] = 0.0;
+        t3[i][0] = t3[i][1] = 0.0;
+      }
+      const int s = seq % WSA;
+      mbar_wait(&full[s], (seq / WSA) & 1);
+      const double2* ps = sm + s * kWApplyStage + 8 * wg + r4;
 #pragma unroll 2
       for (int ms = 0; ms < nm; ms += 4) {
         const int m = ms + c4;
         const bool mok = m < nm;   // contraction padding must be exactly zero
-        double2 av[3], bv[2];
-        double as[3], bs[2];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {   // A[row j = r4][k = c4] = C[row][m]
-          av[i] = (mok && i < cr) ? cs[(8 * (r_lo + i) + r4) * kWCs + m] : make_double2(0.0, 0.0);
-          as[i] = av[i].x + av[i].y;
-        }
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {   // B[k = c4][n = r4] = Phi[m][g]
-          bv[j] = (mok && j < cg) ? ps[m * RSW + 8 * (g_lo + j) + r4] : make_double2(0.0, 0.0);
-          bs[j] = bv[j].x + bv[j].y;
-        }
+        const double2 bv = mok ? ps[m * RSW] : make_double2(0.0, 0.0);   // B[k = c4][n = r4]
+        const double bs = bv.x + bv.y;
         // c phi: re = cr pr - ci pi, im = cr pi + ci pr (3 real products)
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           if (i >= cr) break;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (j >= cg) break;
-            wdmma(t1[i][j][0], t1[i][j][1], av[i].x, bv[j].x);
-            wdmma(t2[i][j][0], t2[i][j][1], av[i].y, bv[j].y);
-            wdmma(t3[i][j][0], t3[i][j][1], as[i], bs[j]);
-          }
+          const double2 av = mok ? cs[(8 * (r_lo + i) + r4) * kWCs + m]   // A[j = r4][k = c4]
+                                 : make_double2(0.0, 0.0);
+          wdmma(t1[i][0], t1[i][1], av.x, bv.x);
+          wdmma(t2[i][0], t2[i][1], av.y, bv.y);
+          wdmma(t3[i][0], t3[i][1], av.x + av.y, bs);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (threadIdx.x == 0 && u + WSA < R.u1) {   // refill once every warp released it
+        mbar_wait(&empty[s], (seq / WSA) & 1);
+        fill(u + WSA, s);
+      }
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         const int row = orow[i];
         if (row < 0) continue;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (j >= cg) break;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const double dr = t1[i][j][h] - t2[i][j][h];
-            const double di = t3[i][j][h] - t1[i][j][h] - t2[i][j][h];
-            Y[(size_t)row * a.nbp + g0 + 8 * (g_lo + j) + 2 * c4 + h] =
-                make_double2(ca * xv[i][j][h].x + cb * dr, ca * xv[i][j][h].y + cb * di);
-          }
+        for (int h = 0; h < 2; ++h) {
+          const double dr = t1[i][h] - t2[i][h];
+          const double di = t3[i][h] - t1[i][h] - t2[i][h];
+          Y[(size_t)row * a.nbp + g0 + 2 * c4 + h] =
+              make_double2(ca * xv[i][h].x + cb * dr, ca * xv[i][h].y + cb * di);
         }
       }
     }

@@ -32,7 +32,9 @@ struct IterCtl {
   ProjTile* tb;    // tiles over rows2
   ProjTile* wa;    // wide tiles (projw.cu) over rows, or null
   ProjTile* wb;    // wide tiles over rows2
+  int wide_min;    // average live rows per wide tile from which the wide path runs
 };
+int projw_min_rows();
 // ints of IterCtl::hdr: [0] na, [1] tiles A, [2] tiles B, [3] rows still iterating,
 // [4] failure flag, [5] loop count, [6] loop cap, [8] wide tiles A, [9] wide tiles B
 constexpr int kHdrInts = 16;

@@ -82,7 +82,7 @@ def main():
         P = dg.pack(list(phi.T))
         lib = _lib.load()
         Y = X.clone()
-        ms_q = timed(torch, lambda: lib.pwb_project_out(ds.handle, 0, rows, ptr(Y)), a.reps)
+        ms_q = timed(torch, lambda: _lib.check(lib.pwb_project_out(ds.handle, 0, rows, ptr(Y))), a.reps)
 
         def zgemm():
             return X - (X @ P.conj().T) @ P
