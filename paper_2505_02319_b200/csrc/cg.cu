@@ -331,6 +331,8 @@ ProjArgs proj_args(pwb_state* st) {
   a.phic_off = as<int>(st->phic_meta) + 2 * st->nk;
   a.phiw = st->wide_ok ? as<double2>(st->phiw) : nullptr;
   a.phiw_off = st->wide_ok ? as<int>(st->phiw_meta) + 2 * st->nk : nullptr;
+  a.phiwa = st->wide_ok ? as<double2>(st->phiwa) : nullptr;
+  a.phiwa_off = st->wide_ok ? as<int>(st->phiwa_meta) + 2 * st->nk : nullptr;
   return a;
 }
 
@@ -350,14 +352,16 @@ static bool use_wide(const pwb_state* st, const ProjPlan& pl, const int* ntiles,
 }
 
 int proj_coeffs_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* X,
-                    double2* part, double2* C, cudaStream_t s, const int* wntiles) {
+                    double2* part, double2* C, cudaStream_t s, const int* wntiles,
+                    long long x_rows) {
   if (!use_wide(st, pl, a.ntiles, wntiles)) return proj_coeffs(pl, a, X, part, C, s);
   if (a.ntiles) PWB_TRY(proj_coeffs(pl, a, X, part, C, s));   // exits when wide is chosen
   ProjArgs w = a;
   w.ntiles = wntiles;
+  if (x_rows <= 0 && !a.rows && pl.max_tiles == 0 && pl.wmax == 0) x_rows = pl.nrows;
   return projw_coeffs(reinterpret_cast<const ProjTile*>(pl.dwtiles.ptr), (int)pl.wtiles.size(),
                       plan_wide_tiles(pl), w, X, part, C,
-                      reinterpret_cast<unsigned*>(pl.wcounters.ptr), s);
+                      reinterpret_cast<unsigned*>(pl.wcounters.ptr), s, x_rows);
 }
 
 int proj_apply_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* C,
@@ -394,7 +398,9 @@ int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* activ
     prof().end(PROF_Q, e, s, pl.nrows);
     return PWB_OK;
   }
-  PWB_TRY(proj_coeffs_any(st, pl, a, X, part, cmat, s, wntiles));
+  // rows allocated in X: the CG buffers hold band_mod rows (stacked x; r: 2 band_mod)
+  const long long x_rows = ntiles ? (long long)band_mod * mult : pl.nrows;
+  PWB_TRY(proj_coeffs_any(st, pl, a, X, part, cmat, s, wntiles, x_rows));
   PWB_TRY(proj_apply_any(st, pl, a, cmat, X, X, 1.0, -1.0, active, band_mod, s, wntiles));
   prof().end(PROF_Q, e, s, prof().rows_hint > 0 ? (long long)mult * prof().rows_hint : pl.nrows);
   return PWB_OK;

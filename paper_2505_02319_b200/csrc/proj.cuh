@@ -15,7 +15,6 @@ constexpr int kProjRowStride = kProjChunk + 4;   // padded smem / chunk-major ro
 constexpr int kProjWideRows = 72;
 constexpr int kProjWideOcc = 72;
 constexpr int kProjWideChunk = 32;
-constexpr int kProjWideStride = kProjWideChunk + 4;
 
 struct ProjTile {
   int row0;   // first row of X in this tile
@@ -38,10 +37,12 @@ struct ProjArgs {
   // orbitals of one chunk are ONE contiguous TMA bulk copy
   const double2* phic;
   const int* phic_off;  // [nk], in double2
-  // the same with 32-coefficient chunks (wide tiles): block k, chunk c, orbital m at
-  // phiw + phiw_off[k] + (c * nocc[k] + m) * kProjWideStride
+  // the same for the wide-tile kernels (projw.cu): coef copy with narrow chunks,
+  // apply copy with 32-coefficient chunks (strides chosen per access pattern)
   const double2* phiw;
   const int* phiw_off;
+  const double2* phiwa;   // the apply kernel's copy (32-wide chunks, stride 38)
+  const int* phiwa_off;
 };
 
 // Build the chunk-major copy of the orbital rows phi [nband][nbp] (k blocks at
@@ -108,14 +109,16 @@ bool projw_enabled();
 int projw_tiles(const std::vector<int>& row_k, std::vector<ProjTile>& out);
 size_t projw_part_elems(int max_tiles);
 // C = Phi^H X over `cap` tiles (device count a.ntiles when set, else nt_host)
+// (x_rows: rows allocated in X, bound of the TMA tensor map; <= 0: per-row copies only)
 int projw_coeffs(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* X,
-                 double2* part, double2* C, unsigned* counters, cudaStream_t st);
+                 double2* part, double2* C, unsigned* counters, cudaStream_t st,
+                 long long x_rows = 0);
 // Y = ca X + cb Phi C
 int projw_apply(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* C,
                 const double2* Xin, double2* Y, double ca, double cb, const int* active,
                 int band_mod, cudaStream_t st);
 int projw_chunked(const double2* phi, int nbp, const std::vector<int>& off_host,
                   const std::vector<int>& nocc_host, DevBuf& phiw, DevBuf& d_meta,
-                  cudaStream_t st);
+                  DevBuf& phiwa, DevBuf& d_meta_a, cudaStream_t st);
 
 }  // namespace pwb

@@ -25,7 +25,11 @@
 // DMMA.8x8x4), so a warp reuses each loaded A fragment across its n
 // fragments and vice versa; complex products use three real DMMAs (Gauss),
 // as in proj.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstring>
+#include <mutex>
 
 #include "proj.cuh"
 #include "tma.cuh"
@@ -34,17 +38,25 @@ namespace pwb {
 
 constexpr int WR = kProjWideRows;    // rows per wide tile (9 n fragments)
 constexpr int WMO = kProjWideOcc;    // orbitals per k block (9 m fragments)
-constexpr int KW = kProjWideChunk;   // coefficients per chunk
-constexpr int RSW = kProjWideStride; // smem / chunk-major row stride (double2): 64 B mod 128 B
-constexpr int NWW = 12;              // compute warps (3 per SM sub-partition)
-constexpr int WST = 2;               // coef pipeline stages
-constexpr int WSA = 3;               // apply pipeline stages
-constexpr int kWCoefStage = (WR + WMO) * RSW;    // double2: X rows, then the Phi block
-constexpr int kWApplyStage = WMO * RSW;          // double2: the Phi block
+#ifndef PWB_WKC
+#define PWB_WKC 32   // coef chunk (coefficients): 2 stages of 83 KB (16 x 4 stages measured 28% slower)
+#endif
+constexpr int KWC = PWB_WKC;             // coef: coefficients per chunk
+constexpr int RSWC = KWC + 4;            // coef smem / chunk-major row stride (double2): the
+                                         // A/B fragment loads (8 rows x 4 columns) need 4 mod 8
+constexpr int KWA = kProjWideChunk;      // apply: coefficients per chunk (32)
+constexpr int RSWA = KWA + 6;            // apply row stride: the B loads (4 rows x 8
+                                         // columns) need 2 or 6 mod 8 (38: conflict-free)
+constexpr int NWW = 12;                  // compute warps (3 per SM sub-partition)
+constexpr int WST = KWC == 16 ? 4 : 2;   // coef pipeline stages
+constexpr int WSA = 3;                   // apply pipeline stages
+constexpr int kWCoefStage = (WR + WMO) * RSWC;   // double2: X rows, then the Phi block
+constexpr int kWApplyStage = WMO * RSWA;         // double2: the Phi block
 constexpr int kWCs = WMO + 4;                    // C tile smem stride (4 mod 8: conflict-free)
 constexpr size_t kWCoefSmem = (size_t)WST * kWCoefStage * 16 + 64;
 constexpr size_t kWApplySmem = (size_t)WSA * kWApplyStage * 16 + (size_t)WR * kWCs * 16 + 64;
 static_assert(kWCoefSmem <= 232448 && kWApplySmem <= 232448, "wide projector smem");
+static_assert(RSWC % 8 == 4 && (RSWA % 8 == 2 || RSWA % 8 == 6), "bank-conflict-free strides");
 constexpr int kWThreads = NWW * 32;
 
 __device__ __forceinline__ void wdmma(double& d0, double& d1, double a, double b) {
@@ -58,9 +70,13 @@ __device__ __forceinline__ int wxrow(const ProjArgs& a, const ProjTile& t, int r
   return a.rows ? a.rows[t.row0 + r] : t.row0 + r;
 }
 
-// chunk-major (32-wide) Phi block: orbitals 0 .. nocc-1 of chunk c of block k
+// chunk-major Phi blocks: orbitals 0 .. nocc-1 of chunk c of block k, in the coef
+// (KWC-wide, stride RSWC) and apply (KWA-wide, stride RSWA) copies
 __device__ __forceinline__ const double2* phiw_at(const ProjArgs& a, int k, int nocc, int c) {
-  return a.phiw + a.phiw_off[k] + (size_t)c * nocc * RSW;
+  return a.phiw + a.phiw_off[k] + (size_t)c * nocc * RSWC;
+}
+__device__ __forceinline__ const double2* phiwa_at(const ProjArgs& a, int k, int nocc, int c) {
+  return a.phiwa + a.phiwa_off[k] + (size_t)c * nocc * RSWA;
 }
 
 // balanced split of n fragments over `parts` warps: [lo, hi) of part p
@@ -73,10 +89,10 @@ struct WRange {
   int u0, u1, nch;   // this CTA's units [u0, u1); chunks per tile
 };
 
-__device__ __forceinline__ WRange wrange(const ProjArgs& a, int nt_host) {
+__device__ __forceinline__ WRange wrange(const ProjArgs& a, int nt_host, int kw) {
   const int ntiles = a.ntiles ? *a.ntiles : nt_host;
   WRange r;
-  r.nch = a.nbp / KW;
+  r.nch = a.nbp / kw;
   const long long units = (long long)ntiles * r.nch;
   const long long per = (units + gridDim.x - 1) / gridDim.x;
   r.u0 = (int)min(units, per * blockIdx.x);
@@ -88,14 +104,15 @@ __device__ __forceinline__ WRange wrange(const ProjArgs& a, int nt_host) {
 __global__ void __launch_bounds__(kWThreads, 1)
     k_projw_coef(ProjArgs a, const double2* __restrict__ X, int nt_host,
                  double2* __restrict__ part, double2* __restrict__ C,
-                 unsigned* __restrict__ counters) {
+                 unsigned* __restrict__ counters, const __grid_constant__ CUtensorMap xmap,
+                 int use_map) {
   pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + WST * kWCoefStage);
   uint64_t* empty = full + WST;
   __shared__ bool last;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const WRange R = wrange(a, nt_host);
+  const WRange R = wrange(a, nt_host, KWC);
   if (threadIdx.x == 0) {
     for (int s = 0; s < WST; ++s) {
       mbar_init(&full[s], 1);
@@ -105,20 +122,31 @@ __global__ void __launch_bounds__(kWThreads, 1)
   }
   __syncthreads();
   if (R.u0 >= R.u1) return;
-  // warp 0 fills stage s with unit u: one Phi block copy + one copy per X row
+  // warp 0 fills stage s with unit u: one Phi block copy, and the tile's X rows as
+  // ONE 2-D tensor copy (box 72 rows x RSWC complex, the smem row stride) when they
+  // are consecutive rows of X, else one bulk copy per row (compacted CG tail)
   auto fill = [&](int u, int s) {
     const int tile = u / R.nch, c = u - tile * R.nch;
     const ProjTile t = a.tiles[tile];
     const int nocc = a.nocc[t.k];
     double2* buf = sm + s * kWCoefStage;
+    const int x0 = wxrow(a, t, 0);
+    const bool box = use_map && wxrow(a, t, t.nrows - 1) - x0 == t.nrows - 1;
     if (lane == 0) {
-      const uint32_t pb = (uint32_t)nocc * RSW * 16;
-      mbar_expect_tx(&full[s], pb + (uint32_t)t.nrows * KW * 16);
-      bulk_g2s(buf + WR * RSW, phiw_at(a, t.k, nocc, c), pb, &full[s]);
+      const uint32_t pb = (uint32_t)nocc * RSWC * 16;
+      mbar_expect_tx(&full[s], pb + (box ? (uint32_t)WR * RSWC * 16 : (uint32_t)t.nrows * KWC * 16));
+      bulk_g2s(buf + WR * RSWC, phiw_at(a, t.k, nocc, c), pb, &full[s]);
+      if (box)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(su32(buf)),
+            "l"(reinterpret_cast<uint64_t>(&xmap)), "r"(2 * KWC * c), "r"(x0), "r"(su32(&full[s]))
+            : "memory");
     }
+    if (box) return;
     __syncwarp();
     for (int r = lane; r < t.nrows; r += 32)
-      bulk_g2s(buf + r * RSW, X + (size_t)wxrow(a, t, r) * a.nbp + (size_t)c * KW, KW * 16,
+      bulk_g2s(buf + r * RSWC, X + (size_t)wxrow(a, t, r) * a.nbp + (size_t)c * KWC, KWC * 16,
                &full[s]);
   };
   if (w == 0)
@@ -148,22 +176,22 @@ __global__ void __launch_bounds__(kWThreads, 1)
       const int s = seq % WST;
       mbar_wait(&full[s], (seq / WST) & 1);
       const double2* xs = sm + s * kWCoefStage;
-      const double2* ps = xs + WR * RSW;
+      const double2* ps = xs + WR * RSWC;
 #pragma unroll 2
-      for (int kk = 0; kk < KW / 4; ++kk) {
+      for (int kk = 0; kk < KWC / 4; ++kk) {
         const int gl = 4 * kk + c4;
         double2 bv[3];
         double bs[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-          bv[j] = j < cn ? xs[(8 * (n_lo + j) + r4) * RSW + gl] : make_double2(0.0, 0.0);
+          bv[j] = j < cn ? xs[(8 * (n_lo + j) + r4) * RSWC + gl] : make_double2(0.0, 0.0);
           bs[j] = bv[j].x + bv[j].y;
         }
         // conj(phi) x: re = pr xr + pi xi, im = pr xi - pi xr (3 real products)
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           if (i >= cm) break;
-          const double2 av = ps[(8 * (m_lo + i) + r4) * RSW + gl];
+          const double2 av = ps[(8 * (m_lo + i) + r4) * RSWC + gl];
           const double ad = av.x - av.y;
 #pragma unroll
           for (int j = 0; j < 3; ++j) {
@@ -254,7 +282,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(cs + WR * kWCs);
   uint64_t* empty = full + WSA;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const WRange R = wrange(a, nt_host);
+  const WRange R = wrange(a, nt_host, KWA);
   if (threadIdx.x == 0) {
     for (int s = 0; s < WSA; ++s) {
       mbar_init(&full[s], 1);
@@ -267,9 +295,9 @@ __global__ void __launch_bounds__(kWThreads, 1)
   auto fill = [&](int u, int s) {   // warp 0, lane 0: the chunk's Phi block
     const int tile = u / R.nch, c = u - tile * R.nch;
     const int k = a.tiles[tile].k, nocc = a.nocc[k];
-    const uint32_t bytes = (uint32_t)nocc * RSW * 16;
+    const uint32_t bytes = (uint32_t)nocc * RSWA * 16;
     mbar_expect_tx(&full[s], bytes);
-    bulk_g2s(sm + s * kWApplyStage, phiw_at(a, k, nocc, c), bytes, &full[s]);
+    bulk_g2s(sm + s * kWApplyStage, phiwa_at(a, k, nocc, c), bytes, &full[s]);
   };
   if (threadIdx.x == 0)
     for (int q = 0; q < WSA && R.u0 + q < R.u1; ++q) fill(R.u0 + q, q);
@@ -299,7 +327,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
     }
     __syncthreads();
     for (; u < uend; ++u, ++seq) {
-      const size_t g0 = (size_t)(u - tile * R.nch) * KW + 8 * wg;
+      const size_t g0 = (size_t)(u - tile * R.nch) * KWA + 8 * wg;
       double2 xv[3][2];   // epilogue X values, loaded while the DMMAs run
 #pragma unroll
       for (int i = 0; i < 3; ++i)
@@ -318,22 +346,37 @@ __global__ void __launch_bounds__(kWThreads, 1)
       const int s = seq % WSA;
       mbar_wait(&full[s], (seq / WSA) & 1);
       const double2* ps = sm + s * kWApplyStage + 8 * wg + r4;
-#pragma unroll 2
-      for (int ms = 0; ms < nm; ms += 4) {
+      // software-pipelined over the orbital steps: the next step's fragments are
+      // loaded from smem before this step's DMMAs issue (3 warps per sub-partition
+      // leave too little parallelism to hide the LDS latency otherwise)
+      auto ldb = [&](int ms) {   // B[k = c4][n = r4] = Phi[m][g]
         const int m = ms + c4;
-        const bool mok = m < nm;   // contraction padding must be exactly zero
-        const double2 bv = mok ? ps[m * RSW] : make_double2(0.0, 0.0);   // B[k = c4][n = r4]
+        return m < nm ? ps[m * RSWA] : make_double2(0.0, 0.0);
+      };
+      auto lda = [&](int ms, int i) {   // A[j = r4][k = c4] = C[row][m]; padding exactly zero
+        const int m = ms + c4;
+        return (m < nm && i < cr) ? cs[(8 * (r_lo + i) + r4) * kWCs + m] : make_double2(0.0, 0.0);
+      };
+      double2 bv = ldb(0), av[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) av[i] = lda(0, i);
+      for (int ms = 0; ms < nm; ms += 4) {
+        const double2 bn = ldb(ms + 4);
+        double2 an[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) an[i] = lda(ms + 4, i);
         const double bs = bv.x + bv.y;
         // c phi: re = cr pr - ci pi, im = cr pi + ci pr (3 real products)
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           if (i >= cr) break;
-          const double2 av = mok ? cs[(8 * (r_lo + i) + r4) * kWCs + m]   // A[j = r4][k = c4]
-                                 : make_double2(0.0, 0.0);
-          wdmma(t1[i][0], t1[i][1], av.x, bv.x);
-          wdmma(t2[i][0], t2[i][1], av.y, bv.y);
-          wdmma(t3[i][0], t3[i][1], av.x + av.y, bs);
+          wdmma(t1[i][0], t1[i][1], av[i].x, bv.x);
+          wdmma(t2[i][0], t2[i][1], av[i].y, bv.y);
+          wdmma(t3[i][0], t3[i][1], av[i].x + av[i].y, bs);
         }
+        bv = bn;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) av[i] = an[i];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -388,15 +431,68 @@ int projw_tiles(const std::vector<int>& row_k, std::vector<ProjTile>& out) {
 
 size_t projw_part_elems(int max_tiles) { return (size_t)(max_tiles + kSM) * WR * WMO; }
 
+// ---- TMA tensor maps of X (2-D FLOAT64 [rows][2 nbp], box 72 rows x 2 RSWC) ----------
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    (void)cudaGetLastError();
+  });
+  return fn;
+}
+
+// cached per (buffer, rows, nbp): the CG buffers are reused every iteration
+static bool x_tensor_map(const double2* X, long long rows, int nbp, CUtensorMap* out) {
+  static thread_local struct Entry {
+    const void* p;
+    long long rows;
+    int nbp;
+    CUtensorMap m;
+  } cache[32];
+  static thread_local int next = 0;
+  static const bool off = getenv("PWB_NO_XMAP") != nullptr;   // A/B measurement
+  if (off || rows <= 0) return false;
+  for (auto& e : cache)
+    if (e.p == X && e.rows == rows && e.nbp == nbp) {
+      *out = e.m;
+      return true;
+    }
+  auto fn = tensor_map_encoder();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)2 * nbp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)nbp * 16};
+  cuuint32_t box[2] = {(cuuint32_t)(2 * RSWC), (cuuint32_t)WR};
+  cuuint32_t es[2] = {1, 1};
+  CUtensorMap m;
+  if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(X), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cache[next] = Entry{X, rows, nbp, m};
+  next = (next + 1) % 32;
+  *out = m;
+  return true;
+}
+
 int projw_coeffs(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* X,
-                 double2* part, double2* C, unsigned* counters, cudaStream_t st) {
+                 double2* part, double2* C, unsigned* counters, cudaStream_t st,
+                 long long x_rows) {
   if (cap == 0) return PWB_OK;
   PWB_TRY(projw_configure());
   a.tiles = dtiles;
-  const long long units = (long long)cap * (a.nbp / KW);
+  const long long units = (long long)cap * (a.nbp / KWC);
   const int grid = (int)std::min<long long>(units, kSM);
+  CUtensorMap xmap;
+  memset(&xmap, 0, sizeof(xmap));
+  const int use_map = x_tensor_map(X, x_rows, a.nbp, &xmap) ? 1 : 0;
   (void)launch_k(k_projw_coef, grid, kWThreads, kWCoefSmem, st, a, X, nt_host, part, C,
-                 counters);
+                 counters, xmap, use_map);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
@@ -407,7 +503,7 @@ int projw_apply(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const 
   if (cap == 0) return PWB_OK;
   PWB_TRY(projw_configure());
   a.tiles = dtiles;
-  const long long units = (long long)cap * (a.nbp / KW);
+  const long long units = (long long)cap * (a.nbp / KWA);
   const int grid = (int)std::min<long long>(units, kSM);
   (void)launch_k(k_projw_apply, grid, kWThreads, kWApplySmem, st, a, C, Xin, Y, ca, cb, active,
                  band_mod > 0 ? band_mod : 1, nt_host);
@@ -415,25 +511,27 @@ int projw_apply(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const 
   return PWB_OK;
 }
 
-// 32-wide chunk-major copy of the orbital rows (one CTA per (orbital row, chunk))
+// chunk-major copy of the orbital rows (one CTA per (orbital row, chunk)): chunk c
+// of orbital m of block k at dst + off[k] + (c * nocc[k] + m) * RS, pads zero
+template <int KC_, int RS_>
 __global__ void k_phiw_chunk(const double2* __restrict__ phi, int nbp, int nk,
                              const int* __restrict__ off, const int* __restrict__ nocc,
-                             const int* __restrict__ phiw_off, double2* __restrict__ phiw) {
+                             const int* __restrict__ dst_off, double2* __restrict__ dst) {
   pdl_wait();
   const int b = blockIdx.x, c = blockIdx.y;
   int k = 0;
   while (k + 1 < nk && off[k + 1] <= b) ++k;
   const int m = b - off[k];
-  double2* dst = phiw + phiw_off[k] + ((size_t)c * nocc[k] + m) * RSW;
-  for (int i = threadIdx.x; i < RSW; i += blockDim.x)
-    dst[i] = i < KW ? phi[(size_t)b * nbp + (size_t)c * KW + i] : make_double2(0.0, 0.0);
+  double2* d = dst + dst_off[k] + ((size_t)c * nocc[k] + m) * RS_;
+  for (int i = threadIdx.x; i < RS_; i += blockDim.x)
+    d[i] = i < KC_ ? phi[(size_t)b * nbp + (size_t)c * KC_ + i] : make_double2(0.0, 0.0);
 }
 
-int projw_chunked(const double2* phi, int nbp, const std::vector<int>& off_host,
-                  const std::vector<int>& nocc_host, DevBuf& phiw, DevBuf& d_meta,
-                  cudaStream_t st) {
-  if (nbp % KW) return fail(PWB_ERR_UNSUPPORTED, "wide projector: row stride not a multiple of 32");
-  const int nk = (int)nocc_host.size(), nchunk = nbp / KW;
+template <int KC_, int RS_>
+static int chunk_copy(const double2* phi, int nbp, const std::vector<int>& off_host,
+                      const std::vector<int>& nocc_host, DevBuf& buf, DevBuf& d_meta,
+                      cudaStream_t st) {
+  const int nk = (int)nocc_host.size(), nchunk = nbp / KC_;
   std::vector<int> meta(3 * nk);
   long long tot = 0;
   int nband = 0;
@@ -441,22 +539,31 @@ int projw_chunked(const double2* phi, int nbp, const std::vector<int>& off_host,
     meta[k] = off_host[k];
     meta[nk + k] = nocc_host[k];
     meta[2 * nk + k] = (int)tot;
-    tot += (long long)nchunk * nocc_host[k] * RSW;
+    tot += (long long)nchunk * nocc_host[k] * RS_;
     nband += nocc_host[k];
   }
   if (tot > 0x7fffffffLL) return fail(PWB_ERR_UNSUPPORTED, "chunk-major orbitals exceed 2^31");
-  PWB_TRY(phiw.ensure((size_t)std::max<long long>(tot, 1) * sizeof(double2)));
+  PWB_TRY(buf.ensure((size_t)std::max<long long>(tot, 1) * sizeof(double2)));
   PWB_TRY(d_meta.ensure(3 * (size_t)nk * sizeof(int)));
   PWB_CUDA(cudaMemcpyAsync(d_meta.ptr, meta.data(), meta.size() * sizeof(int),
                            cudaMemcpyHostToDevice, st));
   const int* dm = as<int>(d_meta);
   if (nband > 0) {
-    (void)launch_k(k_phiw_chunk, dim3(nband, nchunk), 64, 0, st, phi, nbp, nk, dm, dm + nk,
-                   dm + 2 * nk, as<double2>(phiw));
+    (void)launch_k(k_phiw_chunk<KC_, RS_>, dim3(nband, nchunk), 64, 0, st, phi, nbp, nk, dm,
+                   dm + nk, dm + 2 * nk, as<double2>(buf));
     PWB_LAUNCH_CHECK();
   }
   PWB_CUDA(cudaStreamSynchronize(st));   // meta is a host temporary
   return PWB_OK;
+}
+
+int projw_chunked(const double2* phi, int nbp, const std::vector<int>& off_host,
+                  const std::vector<int>& nocc_host, DevBuf& phiw, DevBuf& d_meta,
+                  DevBuf& phiwa, DevBuf& d_meta_a, cudaStream_t st) {
+  if (nbp % KWC || nbp % KWA)
+    return fail(PWB_ERR_UNSUPPORTED, "wide projector: row stride not a multiple of 32");
+  PWB_TRY((chunk_copy<KWC, RSWC>(phi, nbp, off_host, nocc_host, phiw, d_meta, st)));
+  return chunk_copy<KWA, RSWA>(phi, nbp, off_host, nocc_host, phiwa, d_meta_a, st);
 }
 
 }  // namespace pwb

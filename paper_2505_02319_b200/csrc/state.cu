@@ -210,7 +210,7 @@ int pwb_state_create(pwb_grid* g, const int* nocc_per_k, const double* kweight,
   st->wide_ok = ldc <= kProjWideOcc && g->nbp % kProjWideChunk == 0;
   if (st->wide_ok)
     PWB_TRY(projw_chunked(as<double2>(st->phi), g->nbp, st->off, st->nocc, st->phiw,
-                          st->phiw_meta, nullptr));
+                          st->phiw_meta, st->phiwa, st->phiwa_meta, nullptr));
 
   // per-band coefficients [w*2f/sqrt(Omega), w*f', f', w]
   std::vector<double> coef(4 * (size_t)nb);

@@ -78,7 +78,8 @@ int project_rows(pwb_state* st, const ProjPlan& pl, double2* X, const int* activ
 // and plan allow them (device tile counts: a.ntiles for 16-row tiles, wntiles for
 // wide ones), else the 16-row kernels of proj.cu
 int proj_coeffs_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* X,
-                    double2* part, double2* C, cudaStream_t s, const int* wntiles = nullptr);
+                    double2* part, double2* C, cudaStream_t s, const int* wntiles = nullptr,
+                    long long x_rows = 0);
 int proj_apply_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* C,
                    const double2* Xin, double2* Y, double ca, double cb, const int* active,
                    int band_mod, cudaStream_t s, const int* wntiles = nullptr);
@@ -107,7 +108,7 @@ struct pwb_state {
   pwb::DevBuf phi, d_off, d_nocc, d_band_k, d_eps, d_pshift, d_coef, vloc, rho, wt;
   pwb::DevBuf vloct;         // x-major V_local for the fused pencil multiply
   pwb::DevBuf phic, phic_meta;   // chunk-major orbitals for the projector (proj.cuh)
-  pwb::DevBuf phiw, phiw_meta;   // 32-wide chunk-major orbitals (wide tiles, projw.cu)
+  pwb::DevBuf phiw, phiw_meta, phiwa, phiwa_meta;   // chunk-major orbitals of projw.cu
   bool wide_ok = false;          // every k block has <= kProjWideOcc orbitals
   pwb::DevBuf psir;          // psi(r) cache for rows [shard_b0, shard_b1)
   int psir_b0 = -1, psir_b1 = -1;

@@ -191,3 +191,41 @@ def test_gpu_scf_matches_reference_run_scf(name, kw):
     np.testing.assert_allclose(gs.eps[:k], ref.eps[:k], rtol=0, atol=1e-8)
     assert abs(gs.fermi_level - ref.fermi_level) <= 1e-8
     assert rel(gs.rho, ref.rho) < 1e-8
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    import bench
+    return bench.build_workload(2)
+
+
+@pytest.mark.timeout(2400)
+def test_cfg2_metal_slab_solve_matches_oracle(cfg2, pool):
+    """configs[2] (32 x 32 x 320 metal slab, Fermi-Dirac 0.01 Ha, Kerker `pbal`): the
+    occupation-derivative branch (delta eps_F != 0, response.py:131-136) in the RHS chi0
+    and Kerker in the loop (kernels.py:60-79, harness.py:250,272), full solve vs oracle."""
+    import bench
+    from oracle import dyson as od
+    from oracle import outer as oo
+    from oracle import response as orsp
+    from paper_2505_02319_b200.harness import solve_dyson
+    from paper_2505_02319_b200.response import apply_chi0
+    gs, dv0, p = cfg2
+    assert tuple(gs.grids.cube_dims) == (32, 32, 320) and p["strategy"] == "pbal"
+    og = bench.to_oracle(gs)
+    assert abs(float(np.sum(og.fprime_occ()))) > 1e-14 * og.n_occ   # metallic branch active
+    nrm = float(np.linalg.norm(dv0))
+    spec = oo.parse(p["strategy"], p["tau"], p["m"])
+    tols = od.tolerance_vector(og, spec, 0, kv_norm=nrm, rhs_norm=1.0)
+    drho, st = apply_chi0(gs, dv0 / nrm, tols)
+    ref, rst = orsp.chi0(og, dv0 / nrm, tols)
+    assert np.abs(np.array(st.cg_iterations_per_band) - np.array(rst.cg_iterations_per_band)).max() <= 1
+    assert rel(drho, ref) < 1e-8
+    res = solve_dyson(gs, dv0, strategy=p["strategy"], tau=p["tau"], m=p["m"], xc=p["xc"])
+    want = od.solve(og, dv0, spec, xc=p["xc"])
+    assert res.converged and want.converged
+    assert abs(res.iterations - want.iterations) <= 1
+    assert rel(res.solution.cpu().numpy(), want.solution) < 1e-8
+    n = min(len(res.tolerance_schedule), len(want.tolerance_schedule))
+    for got, exp in zip(res.tolerance_schedule[:n], want.tolerance_schedule[:n]):
+        np.testing.assert_allclose(got, exp, rtol=1e-6)
