@@ -454,6 +454,9 @@ __global__ void __launch_bounds__(NT, (N == 96 ? 2 : PWB_PENCIL_H_MINB)) k_penci
 // ~1.9 TB/s.  V(r) is read from L2 in pass B (x-major, coalesced) to leave the
 // shared memory for the stages: 2 CTAs of 9 warps per SM.
 constexpr int kHpStages = 2;
+#ifndef PWB_PENCIL_VPRE
+#define PWB_PENCIL_VPRE 1   // V(r) loads hoisted to the start of pass B
+#endif
 
 template <int N>
 struct PencilHp {
@@ -541,6 +544,20 @@ __global__ void __launch_bounds__(NT + 32, 2) k_pencil_hp(GridDev g, PencilArgs 
     // ---- B: inverse pass 2 -> * V (from L2) -> forward pass 1, in registers
     {
       const int j = tid / LP2, li = tid - j * LP2;
+      // V(r) loads issued first: their L2 latency overlaps the smem reads and the
+      // inverse radix-R2 arithmetic below
+      double vv[MB][R2];
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        const int l = m * LP2 + li;
+#pragma unroll
+        for (int r = 0; r < R2; ++r)
+#if PWB_PENCIL_VPRE
+          vv[m][r] = (l < TC && l < nt) ? __ldg(&a.v[(size_t)(j + r * R1) * nyz + t0 + l]) : 0.0;
+#else
+          vv[m][r] = 0.0;
+#endif
+      }
       double2 v[MB][R2];
 #pragma unroll
       for (int m = 0; m < MB; ++m) {
@@ -563,8 +580,10 @@ __global__ void __launch_bounds__(NT + 32, 2) k_pencil_hp(GridDev g, PencilArgs 
           Dft<R2>::run(v[m], 1.0);
 #pragma unroll
           for (int r = 0; r < R2; ++r) {
-            const double vv = l < nt ? __ldg(&a.v[(size_t)(j + r * R1) * nyz + t0 + l]) : 0.0;
-            v[m][r] = cscale(v[m][r], a.vscale * vv);
+#if !PWB_PENCIL_VPRE
+            vv[m][r] = l < nt ? __ldg(&a.v[(size_t)(j + r * R1) * nyz + t0 + l]) : 0.0;
+#endif
+            v[m][r] = cscale(v[m][r], a.vscale * vv[m][r]);
           }
           Dft<R2>::run(v[m], -1.0);
 #pragma unroll

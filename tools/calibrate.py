@@ -17,6 +17,8 @@ def main():
     p.add_argument("--seed", type=int, default=None)
     p.add_argument("--tol", type=float, default=1e-9)
     p.add_argument("--scan", type=int, default=0, help="scan seeds 0..N-1 at loose tol")
+    p.add_argument("--verbose", action="store_true")
+    p.add_argument("--max-iter", type=int, default=200)
     p.add_argument("--n-electrons", type=int, nargs="*", default=None,
                    help="run the SCF for each of these electron counts (config 2 calibration)")
     args = p.parse_args()
@@ -37,7 +39,8 @@ def main():
             m = replace(model, n_electrons=nel)
             t0 = time.perf_counter()
             try:
-                gs = run_scf_gpu(m, kgrid=spec["params"]["kgrid"], tol=args.tol, verbose=False,
+                gs = run_scf_gpu(m, kgrid=spec["params"]["kgrid"], tol=args.tol,
+                                 verbose=args.verbose, max_iter=args.max_iter,
                                  n_states=nel // 2 + max(6, nel // 4) + 20)
             except Exception as err:  # noqa: BLE001
                 print(f"n_el {nel}: {err}", flush=True)
@@ -46,7 +49,7 @@ def main():
             # N_occ implied by this spectrum for neighbouring electron counts
             occf, _ = smearing_function(m.smearing)
             implied = {}
-            for n2 in range(nel - 16, nel + 17, 2):
+            for n2 in range(max(2, nel - 24), nel + 25, 4):
                 mu, _ = fermi_and_occupations(e, n2, m.temperature, m.smearing)
                 f = occf((e - mu) / m.temperature)
                 implied[n2] = int(np.max(np.nonzero(f > m.occupation_threshold)[0])) + 1
