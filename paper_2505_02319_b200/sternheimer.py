@@ -86,8 +86,12 @@ def solve_sternheimer_many(gs, v_local, bands, rhs_rows, tols, max_iter=None):
     if status == _lib.PWB_ERR_NONCONV:
         bad = int(np.argmax(its < 0))
         # every row iterated until max_iter or convergence; count what was spent
-        limit = int(max_iter) if max_iter else None
-        spent = int(done.sum()) + int(np.sum(its < 0)) * (limit or 0)
+        # (a failed row ran its full budget: max_iter, else 10 n_b of its k block,
+        # sternheimer.py:60-61)
+        failed_k = ds.band_k[bands[its < 0]]
+        limits = (np.full(len(failed_k), int(max_iter)) if max_iter else
+                  10 * np.asarray(ds.grid.nb, dtype=np.int64)[failed_k])
+        spent = int(done.sum()) + int(np.sum(limits))
         ham_counter.add(spent)
         raise NonConvergenceError(
             f"Sternheimer CG for band {int(bands[bad])} stalled at {res[bad]:.3e} "
