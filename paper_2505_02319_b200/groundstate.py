@@ -150,6 +150,9 @@ def external_potential(model, grids):
     v = np.zeros(grids.n_g)
     if not model.gaussians:
         return v
+    a = np.asarray(model.lattice.a, dtype=float)
+    if not np.any(a - np.diag(np.diag(a))):
+        return _external_potential_orthogonal(model, grids)
     pts = grids.real_space_points()
     shifts = _shifts(model.lattice, _cutoff(model))
     for g in model.gaussians:
@@ -158,6 +161,28 @@ def external_potential(model, grids):
             d = pts - (c + s)
             v += g.amplitude * np.exp(-np.einsum("ij,ij->i", d, d) / (2 * g.width ** 2))
     return v
+
+
+def _external_potential_orthogonal(model, grids):
+    """The same lattice sum for an orthogonal cell: the shift set is a product mesh
+    (_shifts) and the Gaussian factorises over the axes, so each well is an outer
+    product of three 1-D image sums.  The point-by-point loop above costs
+    wells x images x N_g (40 x 3645 x 327 680 at configs[2]: ten minutes of host
+    time); this is wells x (images + N) per axis.  Same value up to summation order."""
+    a = np.diag(np.asarray(model.lattice.a, dtype=float))
+    spacing = 2 * np.pi / np.linalg.norm(model.lattice.b, axis=1)
+    lim = np.ceil(_cutoff(model) / spacing).astype(int)
+    v = np.zeros(tuple(grids.cube_dims))
+    for g in model.gaussians:
+        c = np.asarray(g.center, dtype=float) * a
+        f = []
+        for ax in range(3):
+            x = np.arange(grids.cube_dims[ax]) / grids.cube_dims[ax] * a[ax]
+            s = np.arange(-lim[ax], lim[ax] + 1) * a[ax]
+            d = x[:, None] - (c[ax] + s[None, :])
+            f.append(np.exp(-d * d / (2 * g.width ** 2)).sum(axis=1))
+        v += g.amplitude * f[0][:, None, None] * f[1][None, :, None] * f[2][None, None, :]
+    return np.ascontiguousarray(v.ravel(order="F"))
 
 
 def external_potential_derivative(model, grids, index, direction):
