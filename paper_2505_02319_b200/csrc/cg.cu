@@ -337,7 +337,9 @@ ProjArgs proj_args(pwb_state* st) {
 }
 
 int projw_min_rows() {
-  static const int v = getenv("PWB_WIDE_MIN_ROWS") ? atoi(getenv("PWB_WIDE_MIN_ROWS")) : 32;
+  // measured crossover (tools/qmid.py, configs[4] shape, 32 k x 68 orbitals): 16 rows
+  // per k 469 us (16-row pair) vs 552 us (wide), 24 rows per k 843 vs 647 us
+  static const int v = getenv("PWB_WIDE_MIN_ROWS") ? atoi(getenv("PWB_WIDE_MIN_ROWS")) : 20;
   return v;
 }
 

@@ -17,8 +17,8 @@
 //
 // Operands arrive by TMA bulk copies (one copy for the chunk's Phi block from
 // the 32-wide chunk-major copy, one 512 B copy per gathered X row) into an
-// smem ring with full/empty mbarriers; warp 0 refills a stage once every warp
-// has released it (no separate producer warp).  Twelve compute warps -- three
+// smem ring (full mbarriers + a release count per stage); the last warp to
+// release a stage refills it (no separate producer warp, nobody waits).  Twelve compute warps -- three
 // per SM sub-partition, so the four DMMA pipes are loaded evenly (nine warps
 // cap the busiest sub-partition at 3 of 4 warps' worth: 75%) -- form a 4 x 3
 // grid over the output fragments (8 x 8 DMMA tiles, mma.sync.m8n8k4.f64 ->
@@ -85,6 +85,23 @@ __device__ __forceinline__ void splitn(int n, int p, int parts, int& lo, int& hi
   hi = ((p + 1) * n) / parts;
 }
 
+// A warp releases a pipeline stage; true (warp-uniform) for the last of the NWW
+// compute warps of this use of the stage.  Every warp walks the stages in the
+// same order and a stage is refilled only after all of them released it, so a
+// monotonic count suffices.  Replaces an empty-mbarrier that warp 0 had to wait
+// on before refilling: warp 0 is a compute warp too, and its wait for the
+// slowest warp delayed both its own DMMAs and the refill.
+__device__ __forceinline__ bool stage_released(unsigned* count, int lane) {
+  __syncwarp();
+  unsigned old = 0;
+  if (lane == 0) {
+    __threadfence_block();
+    old = atomicAdd(count, 1u);
+  }
+  old = __shfl_sync(0xffffffffu, old, 0);
+  return old % NWW == NWW - 1;
+}
+
 struct WRange {
   int u0, u1, nch;   // this CTA's units [u0, u1); chunks per tile
 };
@@ -109,14 +126,14 @@ __global__ void __launch_bounds__(kWThreads, 1)
   pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + WST * kWCoefStage);
-  uint64_t* empty = full + WST;
   __shared__ bool last;
+  __shared__ unsigned released[WST];   // warps done with a stage (monotonic)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const WRange R = wrange(a, nt_host, KWC);
   if (threadIdx.x == 0) {
     for (int s = 0; s < WST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWW);
+      released[s] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -202,12 +219,8 @@ __global__ void __launch_bounds__(kWThreads, 1)
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (w == 0 && u + WST < R.u1) {   // refill stage s once every warp released it
-        mbar_wait(&empty[s], (seq / WST) & 1);
-        fill(u + WST, s);
-      }
+      // the LAST warp to release stage s refills it (no warp waits for the others)
+      if (stage_released(&released[s], lane) && u + WST < R.u1) fill(u + WST, s);
     }
     // ---- flush the run on `tile`: final C, or a partial + fixed-order reduction
     const int ntiles = a.ntiles ? *a.ntiles : nt_host;
@@ -280,13 +293,13 @@ __global__ void __launch_bounds__(kWThreads, 1)
   extern __shared__ __align__(128) double2 sm[];
   double2* cs = sm + WSA * kWApplyStage;   // C rows of the current tile [WR][kWCs]
   uint64_t* full = reinterpret_cast<uint64_t*>(cs + WR * kWCs);
-  uint64_t* empty = full + WSA;
+  __shared__ unsigned released[WSA];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const WRange R = wrange(a, nt_host, KWA);
   if (threadIdx.x == 0) {
     for (int s = 0; s < WSA; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWW);
+      released[s] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -378,12 +391,8 @@ __global__ void __launch_bounds__(kWThreads, 1)
 #pragma unroll
         for (int i = 0; i < 3; ++i) av[i] = an[i];
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (threadIdx.x == 0 && u + WSA < R.u1) {   // refill once every warp released it
-        mbar_wait(&empty[s], (seq / WSA) & 1);
-        fill(u + WSA, s);
-      }
+      // the last warp to release the stage refills it
+      if (stage_released(&released[s], lane) && lane == 0 && u + WSA < R.u1) fill(u + WSA, s);
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         const int row = orow[i];
