@@ -210,15 +210,30 @@ __global__ void __launch_bounds__(NTC) k_cg_beta(GridDev g, CgScalars sc, int n,
   if (threadIdx.x == 0) sc.rz[row] = rzn;
 }
 
-// One CTA: active flags -> ascending active-row list, the stacked (x; r) list,
-// and the k-grouped projector tiles (<= kProjTileRows rows of one k block).
+// tiles of height T over the stacked span [x rows (c) | r rows (c)] of one k block
+__device__ __forceinline__ int stack_tiles(int c, int T) { return 2 * ((c + T - 1) / T); }
+__device__ __forceinline__ int merged_tiles(int c, int T) { return (2 * c + T - 1) / T; }
+__device__ __forceinline__ void emit_tiles(ProjTile* out, int row0, int c, int T, int k) {
+  for (int j = 0; j * T < c; ++j) out[j] = ProjTile{row0 + T * j, min(T, c - T * j), k};
+}
+__device__ __forceinline__ void emit_stack_tiles(ProjTile* out, int row0, int c, int T, int k) {
+  if (merged_tiles(c, T) < stack_tiles(c, T)) {
+    emit_tiles(out, row0, 2 * c, T, k);
+  } else {
+    emit_tiles(out, row0, c, T, k);
+    emit_tiles(out + (c + T - 1) / T, row0 + c, c, T, k);
+  }
+}
+
+// One CTA: active flags -> ascending active-row list, the k-interleaved stacked
+// (x; r) list, and the k-grouped projector tiles (<= kProjTileRows rows of one k block).
 // Rows are in k-block order, so each k's active rows are contiguous.
 __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __restrict__ active,
                                                   const int* __restrict__ row_k, IterCtl ctl) {
   pdl_wait();
   __shared__ int scan[1024];
   __shared__ int kcnt[kMaxK], kstart[kMaxK], ktile[kMaxK], kwide[kMaxK];
-  __shared__ int wcarry;
+  __shared__ int ktile_b[kMaxK], kwide_b[kMaxK];
   __shared__ int carry;
   const int tid = threadIdx.x;
   for (int k = tid; k < nk; k += 1024) kcnt[k] = 0;
@@ -245,57 +260,56 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
     __syncthreads();
   }
   const int na = carry;
-  for (int j = tid; j < na; j += 1024) {
-    const int r = ctl.rows[j];
-    ctl.rows2[j] = r;
-    ctl.rows2[na + j] = r + n;
-  }
+  // The stacked (x; r) list is k-interleaved: block k holds its x rows, then its r
+  // rows, so ONE tile can carry both where that saves a tile (c live rows on k:
+  // ceil(2c / T) merged tiles against 2 ceil(c / T) separate ones).  In the CG tail,
+  // where c <= 8 on most k, the stacked projection then streams each Phi_k once
+  // instead of twice and fills DMMA fragments that two 4-row tiles would pad.
+  // Where merging saves nothing the x and r spans keep their own tiles (rows
+  // consecutive in X: the wide coef kernel loads such a tile with one TMA box copy).
   if (tid == 0) {
-    int s = 0, t = 0, wt = 0;
+    int s = 0, t = 0, wt = 0, tb = 0, wtb = 0;
     for (int k = 0; k < nk; ++k) {
+      const int c = kcnt[k];
       kstart[k] = s;
       ktile[k] = t;
       kwide[k] = wt;
-      s += kcnt[k];
-      t += (kcnt[k] + kProjTileRows - 1) / kProjTileRows;
-      wt += (kcnt[k] + kProjWideRows - 1) / kProjWideRows;
+      ktile_b[k] = tb;
+      kwide_b[k] = wtb;
+      s += c;
+      t += stack_tiles(c, kProjTileRows) / 2;
+      wt += stack_tiles(c, kProjWideRows) / 2;
+      tb += min(stack_tiles(c, kProjTileRows), merged_tiles(c, kProjTileRows));
+      wtb += min(stack_tiles(c, kProjWideRows), merged_tiles(c, kProjWideRows));
     }
-    // one projector path per iteration: the wide-tile kernels when the live rows
-    // fill the wide tiles (>= wide_min rows per tile on average), else the
-    // 16-row kernels; the other pair is launched too and exits on its zero count
+    // one projector path per call: the wide-tile kernels when the live rows fill the
+    // wide tiles (>= wide_min rows per tile on average), else the 16-row kernels;
+    // the other pair is launched too and exits on its zero count
     const bool wide = ctl.wa != nullptr && wt > 0 && na >= ctl.wide_min * wt;
+    const bool wide_b = ctl.wa != nullptr && wtb > 0 && 2 * na >= ctl.wide_min * wtb;
     ctl.hdr[0] = na;
     ctl.hdr[1] = wide ? 0 : t;
-    ctl.hdr[2] = wide ? 0 : 2 * t;
+    ctl.hdr[2] = wide_b ? 0 : tb;
     ctl.hdr[3] = 0;   // rows still iterating after this iteration (k_cg_resid counts)
     ctl.hdr[8] = wide ? wt : 0;  // wide tiles over rows / over the stacked rows
-    ctl.hdr[9] = wide ? 2 * wt : 0;
-    carry = t;
-    wcarry = wt;
+    ctl.hdr[9] = wide_b ? wtb : 0;
   }
   __syncthreads();
-  const int ntile = carry, nwide = wcarry;
-  if (ctl.wa) {
-    for (int k = tid; k < nk; k += 1024) {
-      const int c = kcnt[k];
-      for (int j = 0; j * kProjWideRows < c; ++j) {
-        ProjTile tl{kstart[k] + kProjWideRows * j, min(kProjWideRows, c - kProjWideRows * j), k};
-        ctl.wa[kwide[k] + j] = tl;
-        ctl.wb[kwide[k] + j] = tl;
-        tl.row0 += na;
-        ctl.wb[nwide + kwide[k] + j] = tl;
-      }
-    }
+  for (int j = tid; j < na; j += 1024) {
+    const int r = ctl.rows[j];
+    const int k = row_k[r];
+    const int q = 2 * kstart[k] + (j - kstart[k]);
+    ctl.rows2[q] = r;
+    ctl.rows2[q + kcnt[k]] = r + n;
   }
   for (int k = tid; k < nk; k += 1024) {
     const int c = kcnt[k];
-    for (int j = 0; j * kProjTileRows < c; ++j) {
-      ProjTile tl{kstart[k] + kProjTileRows * j, min(kProjTileRows, c - kProjTileRows * j), k};
-      ctl.ta[ktile[k] + j] = tl;
-      ctl.tb[ktile[k] + j] = tl;
-      tl.row0 += na;
-      ctl.tb[ntile + ktile[k] + j] = tl;
+    if (ctl.wa) {
+      emit_tiles(ctl.wa + kwide[k], kstart[k], c, kProjWideRows, k);
+      emit_stack_tiles(ctl.wb + kwide_b[k], 2 * kstart[k], c, kProjWideRows, k);
     }
+    emit_tiles(ctl.ta + ktile[k], kstart[k], c, kProjTileRows, k);
+    emit_stack_tiles(ctl.tb + ktile_b[k], 2 * kstart[k], c, kProjTileRows, k);
   }
 }
 

@@ -17,8 +17,8 @@
 //
 // Operands arrive by TMA bulk copies (one copy for the chunk's Phi block from
 // the 32-wide chunk-major copy, one 512 B copy per gathered X row) into an
-// smem ring (full mbarriers + a release count per stage); the last warp to
-// release a stage refills it (no separate producer warp, nobody waits).  Twelve compute warps -- three
+// smem ring with full/empty mbarriers; warp 0 refills a stage once every warp
+// has released it (no separate producer warp).  Twelve compute warps -- three
 // per SM sub-partition, so the four DMMA pipes are loaded evenly (nine warps
 // cap the busiest sub-partition at 3 of 4 warps' worth: 75%) -- form a 4 x 3
 // grid over the output fragments (8 x 8 DMMA tiles, mma.sync.m8n8k4.f64 ->
@@ -85,23 +85,6 @@ __device__ __forceinline__ void splitn(int n, int p, int parts, int& lo, int& hi
   hi = ((p + 1) * n) / parts;
 }
 
-// A warp releases a pipeline stage; true (warp-uniform) for the last of the NWW
-// compute warps of this use of the stage.  Every warp walks the stages in the
-// same order and a stage is refilled only after all of them released it, so a
-// monotonic count suffices.  Replaces an empty-mbarrier that warp 0 had to wait
-// on before refilling: warp 0 is a compute warp too, and its wait for the
-// slowest warp delayed both its own DMMAs and the refill.
-__device__ __forceinline__ bool stage_released(unsigned* count, int lane) {
-  __syncwarp();
-  unsigned old = 0;
-  if (lane == 0) {
-    __threadfence_block();
-    old = atomicAdd(count, 1u);
-  }
-  old = __shfl_sync(0xffffffffu, old, 0);
-  return old % NWW == NWW - 1;
-}
-
 struct WRange {
   int u0, u1, nch;   // this CTA's units [u0, u1); chunks per tile
 };
@@ -126,14 +109,14 @@ __global__ void __launch_bounds__(kWThreads, 1)
   pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + WST * kWCoefStage);
+  uint64_t* empty = full + WST;
   __shared__ bool last;
-  __shared__ unsigned released[WST];   // warps done with a stage (monotonic)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const WRange R = wrange(a, nt_host, KWC);
   if (threadIdx.x == 0) {
     for (int s = 0; s < WST; ++s) {
       mbar_init(&full[s], 1);
-      released[s] = 0u;
+      mbar_init(&empty[s], NWW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -141,30 +124,48 @@ __global__ void __launch_bounds__(kWThreads, 1)
   if (R.u0 >= R.u1) return;
   // warp 0 fills stage s with unit u: one Phi block copy, and the tile's X rows as
   // ONE 2-D tensor copy (box 72 rows x RSWC complex, the smem row stride) when they
-  // are consecutive rows of X, else one bulk copy per row (compacted CG tail)
+  // are consecutive rows of X, else one bulk copy per row (compacted CG tail).
+  // The tile's metadata (tile entry, N_occ, row indices: a chain of dependent global
+  // loads) is fetched once per TILE, not per unit: warp 0 is a compute warp too, and
+  // ~1 us of load latency per fill sat on every stage's critical path.
+  int f_tile = -1, f_nocc = 0, f_x0 = 0, f_rows[3] = {0, 0, 0};
+  ProjTile f_t{0, 0, 0};
+  bool f_box = false;
   auto fill = [&](int u, int s) {
     const int tile = u / R.nch, c = u - tile * R.nch;
-    const ProjTile t = a.tiles[tile];
-    const int nocc = a.nocc[t.k];
+    if (tile != f_tile) {
+      f_tile = tile;
+      f_t = a.tiles[tile];
+      f_nocc = a.nocc[f_t.k];
+      f_x0 = wxrow(a, f_t, 0);
+      f_box = use_map && wxrow(a, f_t, f_t.nrows - 1) - f_x0 == f_t.nrows - 1;
+      if (!f_box)
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          f_rows[q] = lane + 32 * q < f_t.nrows ? wxrow(a, f_t, lane + 32 * q) : 0;
+    }
     double2* buf = sm + s * kWCoefStage;
-    const int x0 = wxrow(a, t, 0);
-    const bool box = use_map && wxrow(a, t, t.nrows - 1) - x0 == t.nrows - 1;
     if (lane == 0) {
-      const uint32_t pb = (uint32_t)nocc * RSWC * 16;
-      mbar_expect_tx(&full[s], pb + (box ? (uint32_t)WR * RSWC * 16 : (uint32_t)t.nrows * KWC * 16));
-      bulk_g2s(buf + WR * RSWC, phiw_at(a, t.k, nocc, c), pb, &full[s]);
-      if (box)
+      const uint32_t pb = (uint32_t)f_nocc * RSWC * 16;
+      mbar_expect_tx(&full[s],
+                     pb + (f_box ? (uint32_t)WR * RSWC * 16 : (uint32_t)f_t.nrows * KWC * 16));
+      bulk_g2s(buf + WR * RSWC, phiw_at(a, f_t.k, f_nocc, c), pb, &full[s]);
+      if (f_box)
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(su32(buf)),
-            "l"(reinterpret_cast<uint64_t>(&xmap)), "r"(2 * KWC * c), "r"(x0), "r"(su32(&full[s]))
+            "l"(reinterpret_cast<uint64_t>(&xmap)), "r"(2 * KWC * c), "r"(f_x0), "r"(su32(&full[s]))
             : "memory");
     }
-    if (box) return;
+    if (f_box) return;
     __syncwarp();
-    for (int r = lane; r < t.nrows; r += 32)
-      bulk_g2s(buf + r * RSWC, X + (size_t)wxrow(a, t, r) * a.nbp + (size_t)c * KWC, KWC * 16,
-               &full[s]);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int r = lane + 32 * q;
+      if (r < f_t.nrows)
+        bulk_g2s(buf + r * RSWC, X + (size_t)f_rows[q] * a.nbp + (size_t)c * KWC, KWC * 16,
+                 &full[s]);
+    }
   };
   if (w == 0)
     for (int q = 0; q < WST && R.u0 + q < R.u1; ++q) fill(R.u0 + q, q);
@@ -219,8 +220,12 @@ __global__ void __launch_bounds__(kWThreads, 1)
           }
         }
       }
-      // the LAST warp to release stage s refills it (no warp waits for the others)
-      if (stage_released(&released[s], lane) && u + WST < R.u1) fill(u + WST, s);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (w == 0 && u + WST < R.u1) {   // refill stage s once every warp released it
+        mbar_wait(&empty[s], (seq / WST) & 1);
+        fill(u + WST, s);
+      }
     }
     // ---- flush the run on `tile`: final C, or a partial + fixed-order reduction
     const int ntiles = a.ntiles ? *a.ntiles : nt_host;
@@ -293,24 +298,29 @@ __global__ void __launch_bounds__(kWThreads, 1)
   extern __shared__ __align__(128) double2 sm[];
   double2* cs = sm + WSA * kWApplyStage;   // C rows of the current tile [WR][kWCs]
   uint64_t* full = reinterpret_cast<uint64_t*>(cs + WR * kWCs);
-  __shared__ unsigned released[WSA];
+  uint64_t* empty = full + WSA;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const WRange R = wrange(a, nt_host, KWA);
   if (threadIdx.x == 0) {
     for (int s = 0; s < WSA; ++s) {
       mbar_init(&full[s], 1);
-      released[s] = 0u;
+      mbar_init(&empty[s], NWW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   if (R.u0 >= R.u1) return;
-  auto fill = [&](int u, int s) {   // warp 0, lane 0: the chunk's Phi block
+  int f_tile = -1, f_k = 0, f_nocc = 0;   // per-tile metadata, fetched once per tile
+  auto fill = [&](int u, int s) {         // warp 0, lane 0: the chunk's Phi block
     const int tile = u / R.nch, c = u - tile * R.nch;
-    const int k = a.tiles[tile].k, nocc = a.nocc[k];
-    const uint32_t bytes = (uint32_t)nocc * RSWA * 16;
+    if (tile != f_tile) {
+      f_tile = tile;
+      f_k = a.tiles[tile].k;
+      f_nocc = a.nocc[f_k];
+    }
+    const uint32_t bytes = (uint32_t)f_nocc * RSWA * 16;
     mbar_expect_tx(&full[s], bytes);
-    bulk_g2s(sm + s * kWApplyStage, phiwa_at(a, k, nocc, c), bytes, &full[s]);
+    bulk_g2s(sm + s * kWApplyStage, phiwa_at(a, f_k, f_nocc, c), bytes, &full[s]);
   };
   if (threadIdx.x == 0)
     for (int q = 0; q < WSA && R.u0 + q < R.u1; ++q) fill(R.u0 + q, q);
@@ -391,8 +401,12 @@ __global__ void __launch_bounds__(kWThreads, 1)
 #pragma unroll
         for (int i = 0; i < 3; ++i) av[i] = an[i];
       }
-      // the last warp to release the stage refills it
-      if (stage_released(&released[s], lane) && lane == 0 && u + WSA < R.u1) fill(u + WSA, s);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (threadIdx.x == 0 && u + WSA < R.u1) {   // refill once every warp released it
+        mbar_wait(&empty[s], (seq / WSA) & 1);
+        fill(u + WSA, s);
+      }
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         const int row = orow[i];

@@ -27,7 +27,7 @@ struct CgScalars {
 struct IterCtl {
   int* hdr;        // [0] na, [1] tiles A, [2] tiles B, [3] active count, [4] fail flag
   int* rows;       // [n]   active rows, ascending
-  int* rows2;      // [2n]  rows then rows + n (stacked (x; r) buffer)
+  int* rows2;      // [2n]  stacked (x; r) buffer rows, k-interleaved: per k its rows, then its rows + n
   ProjTile* ta;    // tiles over rows
   ProjTile* tb;    // tiles over rows2
   ProjTile* wa;    // wide tiles (projw.cu) over rows, or null
