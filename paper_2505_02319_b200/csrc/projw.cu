@@ -85,6 +85,87 @@ __device__ __forceinline__ void splitn(int n, int p, int parts, int& lo, int& hi
   hi = ((p + 1) * n) / parts;
 }
 
+// TMA tensor maps of X, one per box height 8, 16, ..., 72 rows: a tile is loaded
+// with the box of its own height.  (One 72-row box for every tile made the TMA unit
+// move 41 KB of X per stage whatever the tile held -- 72 rows of 576 B each; at
+// 24-48 rows per tile that copy, not the DMMAs, set the stage time:
+// tools/qmid.py, 48 rows per k cost what 66 did.)
+struct XMaps {
+  CUtensorMap m[WR / 8];
+};
+
+// One 32-coefficient chunk of a warp's CM x CN output fragments (coef kernel).  The
+// fragment counts are template parameters: with runtime bounds and `break`s in the
+// unrolled loops nvcc kept the branch for the first fragment but ran the second and
+// third speculatively (DMMAs have no side effects), so a 48-row tile (2 n fragments
+// per warp) executed the DMMAs of a 72-row one (ncu: 31.1 M DMMA at 48 and at 66 rows).
+template <int CM, int CN>
+__device__ __forceinline__ void coef_chunk(const double2* __restrict__ xb,
+                                           const double2* __restrict__ pb, double (&t1)[3][3][2],
+                                           double (&t2)[3][3][2], double (&t3)[3][3][2]) {
+#pragma unroll 2
+  for (int kk = 0; kk < KWC / 4; ++kk) {
+    double2 bv[CN];
+    double bs[CN];
+#pragma unroll
+    for (int j = 0; j < CN; ++j) {
+      bv[j] = xb[8 * j * RSWC + 4 * kk];
+      bs[j] = bv[j].x + bv[j].y;
+    }
+    // conj(phi) x: re = pr xr + pi xi, im = pr xi - pi xr (3 real products)
+#pragma unroll
+    for (int i = 0; i < CM; ++i) {
+      const double2 av = pb[8 * i * RSWC + 4 * kk];
+      const double ad = av.x - av.y;
+#pragma unroll
+      for (int j = 0; j < CN; ++j) {
+        wdmma(t1[i][j][0], t1[i][j][1], av.x, bv[j].x);
+        wdmma(t2[i][j][0], t2[i][j][1], av.y, bv[j].y);
+        wdmma(t3[i][j][0], t3[i][j][1], ad, bs[j]);
+      }
+    }
+  }
+}
+
+// One 32-coefficient chunk of a warp's CR row fragments x one g fragment (apply
+// kernel), software-pipelined over the orbital steps: the next step's fragments are
+// loaded from smem before this step's DMMAs issue (3 warps per sub-partition leave
+// too little parallelism to hide the LDS latency otherwise).
+template <int CR>
+__device__ __forceinline__ void apply_chunk(const double2* __restrict__ ps,
+                                            const double2* __restrict__ ca, int nm, int c4,
+                                            double (&t1)[3][2], double (&t2)[3][2],
+                                            double (&t3)[3][2]) {
+  auto ldb = [&](int ms) {   // B[k = c4][n = r4] = Phi[m][g]
+    const int m = ms + c4;
+    return m < nm ? ps[m * RSWA] : make_double2(0.0, 0.0);
+  };
+  auto lda = [&](int ms, int i) {   // A[j = r4][k = c4] = C[row][m]; padding exactly zero
+    const int m = ms + c4;
+    return m < nm ? ca[8 * i * kWCs + m] : make_double2(0.0, 0.0);
+  };
+  double2 bv = ldb(0), av[CR];
+#pragma unroll
+  for (int i = 0; i < CR; ++i) av[i] = lda(0, i);
+  for (int ms = 0; ms < nm; ms += 4) {
+    const double2 bn = ldb(ms + 4);
+    double2 an[CR];
+#pragma unroll
+    for (int i = 0; i < CR; ++i) an[i] = lda(ms + 4, i);
+    const double bs = bv.x + bv.y;
+    // c phi: re = cr pr - ci pi, im = cr pi + ci pr (3 real products)
+#pragma unroll
+    for (int i = 0; i < CR; ++i) {
+      wdmma(t1[i][0], t1[i][1], av[i].x, bv.x);
+      wdmma(t2[i][0], t2[i][1], av[i].y, bv.y);
+      wdmma(t3[i][0], t3[i][1], av[i].x + av[i].y, bs);
+    }
+    bv = bn;
+#pragma unroll
+    for (int i = 0; i < CR; ++i) av[i] = an[i];
+  }
+}
+
 struct WRange {
   int u0, u1, nch;   // this CTA's units [u0, u1); chunks per tile
 };
@@ -104,7 +185,7 @@ __device__ __forceinline__ WRange wrange(const ProjArgs& a, int nt_host, int kw)
 __global__ void __launch_bounds__(kWThreads, 1)
     k_projw_coef(ProjArgs a, const double2* __restrict__ X, int nt_host,
                  double2* __restrict__ part, double2* __restrict__ C,
-                 unsigned* __restrict__ counters, const __grid_constant__ CUtensorMap xmap,
+                 unsigned* __restrict__ counters, const __grid_constant__ XMaps xmaps,
                  int use_map) {
   pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
@@ -147,14 +228,16 @@ __global__ void __launch_bounds__(kWThreads, 1)
     double2* buf = sm + s * kWCoefStage;
     if (lane == 0) {
       const uint32_t pb = (uint32_t)f_nocc * RSWC * 16;
-      mbar_expect_tx(&full[s],
-                     pb + (f_box ? (uint32_t)WR * RSWC * 16 : (uint32_t)f_t.nrows * KWC * 16));
+      const int hb = (f_t.nrows + 7) >> 3;   // box height in fragments: the map of that height
+      mbar_expect_tx(&full[s], pb + (f_box ? (uint32_t)(8 * hb) * RSWC * 16
+                                           : (uint32_t)f_t.nrows * KWC * 16));
       bulk_g2s(buf + WR * RSWC, phiw_at(a, f_t.k, f_nocc, c), pb, &full[s]);
       if (f_box)
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(su32(buf)),
-            "l"(reinterpret_cast<uint64_t>(&xmap)), "r"(2 * KWC * c), "r"(f_x0), "r"(su32(&full[s]))
+            "l"(reinterpret_cast<uint64_t>(&xmaps.m[hb - 1])), "r"(2 * KWC * c), "r"(f_x0),
+            "r"(su32(&full[s]))
             : "memory");
     }
     if (f_box) return;
@@ -195,29 +278,20 @@ __global__ void __launch_bounds__(kWThreads, 1)
       mbar_wait(&full[s], (seq / WST) & 1);
       const double2* xs = sm + s * kWCoefStage;
       const double2* ps = xs + WR * RSWC;
-#pragma unroll 2
-      for (int kk = 0; kk < KWC / 4; ++kk) {
-        const int gl = 4 * kk + c4;
-        double2 bv[3];
-        double bs[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          bv[j] = j < cn ? xs[(8 * (n_lo + j) + r4) * RSWC + gl] : make_double2(0.0, 0.0);
-          bs[j] = bv[j].x + bv[j].y;
-        }
-        // conj(phi) x: re = pr xr + pi xi, im = pr xi - pi xr (3 real products)
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          if (i >= cm) break;
-          const double2 av = ps[(8 * (m_lo + i) + r4) * RSWC + gl];
-          const double ad = av.x - av.y;
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            if (j >= cn) break;
-            wdmma(t1[i][j][0], t1[i][j][1], av.x, bv[j].x);
-            wdmma(t2[i][j][0], t2[i][j][1], av.y, bv[j].y);
-            wdmma(t3[i][j][0], t3[i][j][1], ad, bs[j]);
-          }
+      {
+        const double2* xb = xs + (8 * n_lo + r4) * RSWC + c4;
+        const double2* pb = ps + (8 * m_lo + r4) * RSWC + c4;
+        switch (4 * cm + cn) {   // warp-uniform; one straight-line body per fragment count
+          case 4 * 1 + 1: coef_chunk<1, 1>(xb, pb, t1, t2, t3); break;
+          case 4 * 1 + 2: coef_chunk<1, 2>(xb, pb, t1, t2, t3); break;
+          case 4 * 1 + 3: coef_chunk<1, 3>(xb, pb, t1, t2, t3); break;
+          case 4 * 2 + 1: coef_chunk<2, 1>(xb, pb, t1, t2, t3); break;
+          case 4 * 2 + 2: coef_chunk<2, 2>(xb, pb, t1, t2, t3); break;
+          case 4 * 2 + 3: coef_chunk<2, 3>(xb, pb, t1, t2, t3); break;
+          case 4 * 3 + 1: coef_chunk<3, 1>(xb, pb, t1, t2, t3); break;
+          case 4 * 3 + 2: coef_chunk<3, 2>(xb, pb, t1, t2, t3); break;
+          case 4 * 3 + 3: coef_chunk<3, 3>(xb, pb, t1, t2, t3); break;
+          default: break;   // this warp has no fragment of the tile
         }
       }
       __syncwarp();
@@ -369,37 +443,14 @@ __global__ void __launch_bounds__(kWThreads, 1)
       const int s = seq % WSA;
       mbar_wait(&full[s], (seq / WSA) & 1);
       const double2* ps = sm + s * kWApplyStage + 8 * wg + r4;
-      // software-pipelined over the orbital steps: the next step's fragments are
-      // loaded from smem before this step's DMMAs issue (3 warps per sub-partition
-      // leave too little parallelism to hide the LDS latency otherwise)
-      auto ldb = [&](int ms) {   // B[k = c4][n = r4] = Phi[m][g]
-        const int m = ms + c4;
-        return m < nm ? ps[m * RSWA] : make_double2(0.0, 0.0);
-      };
-      auto lda = [&](int ms, int i) {   // A[j = r4][k = c4] = C[row][m]; padding exactly zero
-        const int m = ms + c4;
-        return (m < nm && i < cr) ? cs[(8 * (r_lo + i) + r4) * kWCs + m] : make_double2(0.0, 0.0);
-      };
-      double2 bv = ldb(0), av[3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) av[i] = lda(0, i);
-      for (int ms = 0; ms < nm; ms += 4) {
-        const double2 bn = ldb(ms + 4);
-        double2 an[3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) an[i] = lda(ms + 4, i);
-        const double bs = bv.x + bv.y;
-        // c phi: re = cr pr - ci pi, im = cr pi + ci pr (3 real products)
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          if (i >= cr) break;
-          wdmma(t1[i][0], t1[i][1], av[i].x, bv.x);
-          wdmma(t2[i][0], t2[i][1], av[i].y, bv.y);
-          wdmma(t3[i][0], t3[i][1], av[i].x + av[i].y, bs);
+      {
+        const double2* ca = cs + (8 * r_lo + r4) * kWCs;
+        switch (cr) {   // warp-uniform; see coef_chunk for why the count is a template
+          case 1: apply_chunk<1>(ps, ca, nm, c4, t1, t2, t3); break;
+          case 2: apply_chunk<2>(ps, ca, nm, c4, t1, t2, t3); break;
+          case 3: apply_chunk<3>(ps, ca, nm, c4, t1, t2, t3); break;
+          default: break;
         }
-        bv = bn;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) av[i] = an[i];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -471,12 +522,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // cached per (buffer, rows, nbp): the CG buffers are reused every iteration
-static bool x_tensor_map(const double2* X, long long rows, int nbp, CUtensorMap* out) {
+static bool x_tensor_maps(const double2* X, long long rows, int nbp, XMaps* out) {
   static thread_local struct Entry {
     const void* p;
     long long rows;
     int nbp;
-    CUtensorMap m;
+    XMaps m;
   } cache[32];
   static thread_local int next = 0;
   static const bool off = getenv("PWB_NO_XMAP") != nullptr;   // A/B measurement
@@ -490,13 +541,15 @@ static bool x_tensor_map(const double2* X, long long rows, int nbp, CUtensorMap*
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)2 * nbp, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)nbp * 16};
-  cuuint32_t box[2] = {(cuuint32_t)(2 * RSWC), (cuuint32_t)WR};
   cuuint32_t es[2] = {1, 1};
-  CUtensorMap m;
-  if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(X), dims, strides, box, es,
-         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
+  XMaps m;
+  for (int h = 0; h < WR / 8; ++h) {
+    cuuint32_t box[2] = {(cuuint32_t)(2 * RSWC), (cuuint32_t)(8 * (h + 1))};
+    if (fn(&m.m[h], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(X), dims, strides,
+           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
   cache[next] = Entry{X, rows, nbp, m};
   next = (next + 1) % 32;
   *out = m;
@@ -511,11 +564,11 @@ int projw_coeffs(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const
   a.tiles = dtiles;
   const long long units = (long long)cap * (a.nbp / KWC);
   const int grid = (int)std::min<long long>(units, kSM);
-  CUtensorMap xmap;
-  memset(&xmap, 0, sizeof(xmap));
-  const int use_map = x_tensor_map(X, x_rows, a.nbp, &xmap) ? 1 : 0;
+  XMaps xmaps;
+  memset(&xmaps, 0, sizeof(xmaps));
+  const int use_map = x_tensor_maps(X, x_rows, a.nbp, &xmaps) ? 1 : 0;
   (void)launch_k(k_projw_coef, grid, kWThreads, kWCoefSmem, st, a, X, nt_host, part, C,
-                 counters, xmap, use_map);
+                 counters, xmaps, use_map);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
