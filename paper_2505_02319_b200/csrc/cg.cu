@@ -351,9 +351,12 @@ ProjArgs proj_args(pwb_state* st) {
 }
 
 int projw_min_rows() {
-  // measured crossover (tools/qmid.py, configs[4] shape, 32 k x 68 orbitals): 16 rows
-  // per k 469 us (16-row pair) vs 552 us (wide), 24 rows per k 843 vs 647 us
-  static const int v = getenv("PWB_WIDE_MIN_ROWS") ? atoi(getenv("PWB_WIDE_MIN_ROWS")) : 20;
+  // Average live rows per wide tile from which the wide-tile kernels run.  Since the
+  // inner loops take their fragment counts as template parameters the wide pair wins
+  // at every width (tools/qmid.py, configs[4] shape: 1 row on 1 k 30.0 vs 33.8 us,
+  // 4 rows on each of 32 k 284 vs 355 us, 16 rows per k 409 vs 433 us), so the 16-row
+  // pair only serves states with more than 72 orbitals per k.
+  static const int v = getenv("PWB_WIDE_MIN_ROWS") ? atoi(getenv("PWB_WIDE_MIN_ROWS")) : 1;
   return v;
 }
 
