@@ -238,7 +238,9 @@ def projector_roofline(prof, gs, peak_fp64):
     shares, frac = _shares(prof)
     per, src = _traffic(blocks[0].grids.cube_dims, "projector")
     rows = units / max(count, 1)
-    return {"kernel": "projector Q X (k_proj_coef + k_proj_apply), all CG calls of one solve",
+    wide = float(nocc.max()) <= 72   # projw.cu serves N_occ,k <= 72, proj.cu the rest
+    pair = "k_projw_coef + k_projw_apply" if wide else "k_proj_coef + k_proj_apply"
+    return {"kernel": f"projector Q X ({pair}), all CG calls of one solve",
             "bound": "tensor", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s (FP64)",
             "frac": achieved / peak_fp64, "traffic": per * rows if per else None,
             "traffic_source": src,
