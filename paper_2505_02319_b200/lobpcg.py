@@ -170,7 +170,7 @@ def _density(kb, X, occ_w):
 
 def run_scf_gpu(model, kgrid=(1, 1, 1), tol=1e-9, max_iter=200, kerker_alpha=0.8, damping=0.8,
                 n_states=None, eig_tol=1e-9, verbose=False, seed=0, mixing="anderson",
-                history=8):
+                history=8, converge_kept=False):
     """k-point SCF on the GPU; returns a KGroundState (or GroundState for Gamma only).
 
     The fixed point is the reference's (groundstate.py:333-394: same density,
@@ -179,6 +179,11 @@ def run_scf_gpu(model, kgrid=(1, 1, 1), tol=1e-9, max_iter=200, kerker_alpha=0.8
     "anderson" (default) Anderson/Pulay extrapolation over the last `history`
     steps with the same Kerker-preconditioned damped step -- the metal slab
     (configs[2]) does not converge in 200 plain Kerker steps.
+
+    converge_kept: also converge the kept unoccupied bands (max(3, 10% of N_occ)
+    above N_occ) to eig_tol in the final diagonalisation; by default only the
+    occupied bands and eps_{N_occ+1} gate it.  schur.solve_sternheimer_schur
+    needs them converged.
     """
     torch = torch_mod()
     kfr = monkhorst_pack(kgrid) if np.ndim(kgrid) == 1 else np.asarray(kgrid, dtype=float)
@@ -237,6 +242,9 @@ def run_scf_gpu(model, kgrid=(1, 1, 1), tol=1e-9, max_iter=200, kerker_alpha=0.8
             print(f"gpu-scf {it:3d} res {res:.3e} mu {mu:+.6f} nocc {nocc} eig_tol {etol:.1e}",
                   flush=True)
         if res <= tol:
+            if converge_kept:
+                top = max(nocc)
+                n_check = min(kb.nst, top + max(3, int(np.ceil(0.1 * top))))
             eps, X, eres = lobpcg(kb, vloc, X, tol=eig_tol, n_check=n_check)
             mu, _ = fermi_and_occupations(eps.reshape(-1), model.n_electrons, model.temperature,
                                           model.smearing, np.repeat(wk, kb.nst))
