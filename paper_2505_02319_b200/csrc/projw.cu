@@ -300,7 +300,11 @@ __device__ __forceinline__ void projw_coef_body(const ProjArgs& a, const double2
       {
         const double2* xb = xs + (8 * n_lo + r4) * RSWC + c4;
         const double2* pb = ps + (8 * m_lo + r4) * RSWC + c4;
+#ifdef PWB_EXP_NOCOMPUTE   // experiment: pipeline structure only (results are garbage)
+        switch (0) {
+#else
         switch (4 * cm + cn) {   // warp-uniform; one straight-line body per fragment count
+#endif
           case 4 * 1 + 1: coef_chunk<1, 1>(xb, pb, t1, t2, t3); break;
           case 4 * 1 + 2: coef_chunk<1, 2>(xb, pb, t1, t2, t3); break;
           case 4 * 1 + 3: coef_chunk<1, 3>(xb, pb, t1, t2, t3); break;
@@ -489,7 +493,11 @@ __device__ __forceinline__ void projw_apply_body(const ProjArgs& a, const double
       const double2* ps = ring + s * kWApplyStage + 8 * wg + r4;
       {
         const double2* ca = cs + (8 * r_lo + r4) * kWCs;
+#ifdef PWB_EXP_NOCOMPUTE
+        switch (0) {
+#else
         switch (cr) {   // warp-uniform; see coef_chunk for why the count is a template
+#endif
           case 1: apply_chunk<1>(ps, ca, nm, c4, t1, t2, t3); break;
           case 2: apply_chunk<2>(ps, ca, nm, c4, t1, t2, t3); break;
           case 3: apply_chunk<3>(ps, ca, nm, c4, t1, t2, t3); break;
