@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
   // Where merging saves nothing the x and r spans keep their own tiles (rows
   // consecutive in X: the wide coef kernel loads such a tile with one TMA box copy).
   if (tid == 0) {
-    int s = 0, t = 0, wt = 0, tb = 0, wtb = 0, mra = 0, mrb = 0;
+    int s = 0, t = 0, wt = 0, tb = 0, wtb = 0;
     for (int k = 0; k < nk; ++k) {
       const int c = kcnt[k];
       kstart[k] = s;
@@ -281,9 +281,6 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
       wt += stack_tiles(c, kProjWideRows) / 2;
       tb += min(stack_tiles(c, kProjTileRows), merged_tiles(c, kProjTileRows));
       wtb += min(stack_tiles(c, kProjWideRows), merged_tiles(c, kProjWideRows));
-      mra = max(mra, min(c, kProjWideRows));
-      mrb = max(mrb, merged_tiles(c, kProjWideRows) < stack_tiles(c, kProjWideRows)
-                         ? min(2 * c, kProjWideRows) : min(c, kProjWideRows));
     }
     // one projector path per call: the wide-tile kernels when the live rows fill the
     // wide tiles (>= wide_min rows per tile on average), else the 16-row kernels;
@@ -296,8 +293,6 @@ __global__ void __launch_bounds__(1024) k_compact(int n, int nk, const int* __re
     ctl.hdr[3] = 0;   // rows still iterating after this iteration (k_cg_resid counts)
     ctl.hdr[8] = wide ? wt : 0;  // wide tiles over rows / over the stacked rows
     ctl.hdr[9] = wide_b ? wtb : 0;
-    ctl.hdr[10] = mra;   // tallest wide tile of each list: the ring depth (projw.cu)
-    ctl.hdr[11] = mrb;
   }
   __syncthreads();
   for (int j = tid; j < na; j += 1024) {
@@ -375,13 +370,6 @@ static bool use_wide(const pwb_state* st, const ProjPlan& pl, const int* ntiles,
   return pl.nrows >= projw_min_rows() * (int)pl.wtiles.size();
 }
 
-// tallest wide tile of a host plan (device plans: k_compact writes it beside the count)
-static int plan_wide_max_rows(const ProjPlan& pl) {
-  int m = 0;
-  for (const ProjTile& t : pl.wtiles) m = std::max(m, t.nrows);
-  return m > 0 ? m : kProjWideRows;
-}
-
 int proj_coeffs_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* X,
                     double2* part, double2* C, cudaStream_t s, const int* wntiles,
                     long long x_rows) {
@@ -392,8 +380,7 @@ int proj_coeffs_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2
   if (x_rows <= 0 && !a.rows && pl.max_tiles == 0 && pl.wmax == 0) x_rows = pl.nrows;
   return projw_coeffs(reinterpret_cast<const ProjTile*>(pl.dwtiles.ptr), (int)pl.wtiles.size(),
                       plan_wide_tiles(pl), w, X, part, C,
-                      reinterpret_cast<unsigned*>(pl.wcounters.ptr), s, x_rows,
-                      plan_wide_max_rows(pl));
+                      reinterpret_cast<unsigned*>(pl.wcounters.ptr), s, x_rows);
 }
 
 int proj_apply_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2* C,
@@ -405,8 +392,7 @@ int proj_apply_any(pwb_state* st, const ProjPlan& pl, ProjArgs a, const double2*
   ProjArgs w = a;
   w.ntiles = wntiles;
   return projw_apply(reinterpret_cast<const ProjTile*>(pl.dwtiles.ptr), (int)pl.wtiles.size(),
-                     plan_wide_tiles(pl), w, C, Xin, Y, ca, cb, active, band_mod, s,
-                     plan_wide_max_rows(pl));
+                     plan_wide_tiles(pl), w, C, Xin, Y, ca, cb, active, band_mod, s);
 }
 
 // Q X in place for the rows of a plan (masked by `active` when given)

@@ -109,16 +109,14 @@ bool projw_enabled();
 int projw_tiles(const std::vector<int>& row_k, std::vector<ProjTile>& out);
 size_t projw_part_elems(int max_tiles);
 // C = Phi^H X over `cap` tiles (device count a.ntiles when set, else nt_host)
-// (x_rows: rows allocated in X, bound of the TMA tensor map; <= 0: per-row copies only;
-// max_rows: tallest tile of a host list -- device plans carry it at a.ntiles[2] --
-// which selects the depth of the smem ring)
+// (x_rows: rows allocated in X, bound of the TMA tensor map; <= 0: per-row copies only)
 int projw_coeffs(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* X,
                  double2* part, double2* C, unsigned* counters, cudaStream_t st,
-                 long long x_rows = 0, int max_rows = kProjWideRows);
+                 long long x_rows = 0);
 // Y = ca X + cb Phi C
 int projw_apply(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* C,
                 const double2* Xin, double2* Y, double ca, double cb, const int* active,
-                int band_mod, cudaStream_t st, int max_rows = kProjWideRows);
+                int band_mod, cudaStream_t st);
 int projw_chunked(const double2* phi, int nbp, const std::vector<int>& off_host,
                   const std::vector<int>& nocc_host, DevBuf& phiw, DevBuf& d_meta,
                   DevBuf& phiwa, DevBuf& d_meta_a, cudaStream_t st);

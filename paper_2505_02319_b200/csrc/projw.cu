@@ -48,31 +48,13 @@ constexpr int KWA = kProjWideChunk;      // apply: coefficients per chunk (32)
 constexpr int RSWA = KWA + 6;            // apply row stride: the B loads (4 rows x 8
                                          // columns) need 2 or 6 mod 8 (38: conflict-free)
 constexpr int NWW = 12;                  // compute warps (3 per SM sub-partition)
-// Pipeline depth follows the tallest tile of a launch (rows rounded up to a
-// fragment; k_compact reports it, host plans know it): a coef stage holds that many
-// X rows + the Phi block, the apply kernel's C tile that many rows, and the ring
-// takes the stages that fit.  Full-height tiles: 2 coef / 3 apply stages; <= 40
-// rows: 3 / 4; <= 16 rows (the CG tail, where the kernels only stream Phi_k from HBM
-// and bytes in flight per SM set the rate): 4 / 4.  The three shapes are template
-// instances, so strides and stage counts stay compile-time constants.
-template <int XR>
-struct WShape {
-  static constexpr int kCoefStage = (XR + WMO) * RSWC;   // double2: X rows, then the Phi block
-  static constexpr int kCoefStages = XR <= 16 ? 4 : XR <= 40 ? 3 : 2;
-  static constexpr int kApplyStages = XR <= 40 ? 4 : 3;
-};
+constexpr int WST = KWC == 16 ? 4 : 2;   // coef pipeline stages
+constexpr int WSA = 3;                   // apply pipeline stages
+constexpr int kWCoefStage = (WR + WMO) * RSWC;   // double2: X rows, then the Phi block
 constexpr int kWApplyStage = WMO * RSWA;         // double2: the Phi block
 constexpr int kWCs = WMO + 4;                    // C tile smem stride (4 mod 8: conflict-free)
-constexpr int kWMaxStages = 4;
-constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
-constexpr int kWCoefRing = cmax3(WShape<16>::kCoefStages * WShape<16>::kCoefStage,
-                                 WShape<40>::kCoefStages * WShape<40>::kCoefStage,
-                                 WShape<WR>::kCoefStages * WShape<WR>::kCoefStage);
-constexpr int kWApplyRing = cmax3(WShape<16>::kApplyStages * kWApplyStage + 16 * kWCs,
-                                  WShape<40>::kApplyStages * kWApplyStage + 40 * kWCs,
-                                  WShape<WR>::kApplyStages * kWApplyStage + WR * kWCs);
-constexpr size_t kWCoefSmem = (size_t)kWCoefRing * 16 + 64;
-constexpr size_t kWApplySmem = (size_t)kWApplyRing * 16 + 64;
+constexpr size_t kWCoefSmem = (size_t)WST * kWCoefStage * 16 + 64;
+constexpr size_t kWApplySmem = (size_t)WSA * kWApplyStage * 16 + (size_t)WR * kWCs * 16 + 64;
 static_assert(kWCoefSmem <= 232448 && kWApplySmem <= 232448, "wide projector smem");
 static_assert(RSWC % 8 == 4 && (RSWA % 8 == 2 || RSWA % 8 == 6), "bank-conflict-free strides");
 constexpr int kWThreads = NWW * 32;
@@ -200,17 +182,16 @@ __device__ __forceinline__ WRange wrange(const ProjArgs& a, int nt_host, int kw)
 }
 
 // ---------------------------------------------------------------------------
-template <int XR>
-__device__ __forceinline__ void projw_coef_body(const ProjArgs& a, const double2* __restrict__ X,
-                                                int nt_host, double2* __restrict__ part,
-                                                double2* __restrict__ C,
-                                                unsigned* __restrict__ counters,
-                                                const XMaps& xmaps, int use_map, double2* sm,
-                                                bool& last) {
-  constexpr int WST = WShape<XR>::kCoefStages;
-  constexpr int kWCoefStage = WShape<XR>::kCoefStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kWCoefRing);
-  uint64_t* empty = full + kWMaxStages;
+__global__ void __launch_bounds__(kWThreads, 1)
+    k_projw_coef(ProjArgs a, const double2* __restrict__ X, int nt_host,
+                 double2* __restrict__ part, double2* __restrict__ C,
+                 unsigned* __restrict__ counters, const __grid_constant__ XMaps xmaps,
+                 int use_map) {
+  pdl_wait();
+  extern __shared__ __align__(128) double2 sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + WST * kWCoefStage);
+  uint64_t* empty = full + WST;
+  __shared__ bool last;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const WRange R = wrange(a, nt_host, KWC);
   if (threadIdx.x == 0) {
@@ -250,7 +231,7 @@ __device__ __forceinline__ void projw_coef_body(const ProjArgs& a, const double2
       const int hb = (f_t.nrows + 7) >> 3;   // box height in fragments: the map of that height
       mbar_expect_tx(&full[s], pb + (f_box ? (uint32_t)(8 * hb) * RSWC * 16
                                            : (uint32_t)f_t.nrows * KWC * 16));
-      bulk_g2s(buf + XR * RSWC, phiw_at(a, f_t.k, f_nocc, c), pb, &full[s]);
+      bulk_g2s(buf + WR * RSWC, phiw_at(a, f_t.k, f_nocc, c), pb, &full[s]);
       if (f_box)
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -296,15 +277,11 @@ __device__ __forceinline__ void projw_coef_body(const ProjArgs& a, const double2
       const int s = seq % WST;
       mbar_wait(&full[s], (seq / WST) & 1);
       const double2* xs = sm + s * kWCoefStage;
-      const double2* ps = xs + XR * RSWC;
+      const double2* ps = xs + WR * RSWC;
       {
         const double2* xb = xs + (8 * n_lo + r4) * RSWC + c4;
         const double2* pb = ps + (8 * m_lo + r4) * RSWC + c4;
-#ifdef PWB_EXP_NOCOMPUTE   // experiment: pipeline structure only (results are garbage)
-        switch (0) {
-#else
         switch (4 * cm + cn) {   // warp-uniform; one straight-line body per fragment count
-#endif
           case 4 * 1 + 1: coef_chunk<1, 1>(xb, pb, t1, t2, t3); break;
           case 4 * 1 + 2: coef_chunk<1, 2>(xb, pb, t1, t2, t3); break;
           case 4 * 1 + 3: coef_chunk<1, 3>(xb, pb, t1, t2, t3); break;
@@ -386,41 +363,16 @@ __device__ __forceinline__ void projw_coef_body(const ProjArgs& a, const double2
   }
 }
 
-// tallest tile of the launch: device plans carry it two ints after the tile count
-// (k_compact: hdr[10] / hdr[11] beside hdr[8] / hdr[9]), host plans pass it
-__device__ __forceinline__ int tallest_tile(const ProjArgs& a, int mr_host) {
-  return a.ntiles ? a.ntiles[2] : mr_host;
-}
-
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWThreads, 1)
-    k_projw_coef(ProjArgs a, const double2* __restrict__ X, int nt_host,
-                 double2* __restrict__ part, double2* __restrict__ C,
-                 unsigned* __restrict__ counters, const __grid_constant__ XMaps xmaps,
-                 int use_map, int mr_host) {
+    k_projw_apply(ProjArgs a, const double2* __restrict__ C, const double2* __restrict__ Xin,
+                  double2* __restrict__ Y, double ca, double cb, const int* __restrict__ active,
+                  int band_mod, int nt_host) {
   pdl_wait();
   extern __shared__ __align__(128) double2 sm[];
-  __shared__ bool last;
-  const int mr = tallest_tile(a, mr_host);
-  if (mr <= 16)
-    projw_coef_body<16>(a, X, nt_host, part, C, counters, xmaps, use_map, sm, last);
-  else if (mr <= 40)
-    projw_coef_body<40>(a, X, nt_host, part, C, counters, xmaps, use_map, sm, last);
-  else
-    projw_coef_body<WR>(a, X, nt_host, part, C, counters, xmaps, use_map, sm, last);
-}
-
-// ---------------------------------------------------------------------------
-template <int XR>
-__device__ __forceinline__ void projw_apply_body(const ProjArgs& a, const double2* __restrict__ C,
-                                                 const double2* __restrict__ Xin,
-                                                 double2* __restrict__ Y, double ca, double cb,
-                                                 const int* __restrict__ active, int band_mod,
-                                                 int nt_host, double2* sm) {
-  constexpr int WSA = WShape<XR>::kApplyStages;
-  double2* cs = sm;                 // C rows of the current tile [XR][kWCs]
-  double2* ring = sm + XR * kWCs;   // then the Phi stages
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kWApplyRing);
-  uint64_t* empty = full + kWMaxStages;
+  double2* cs = sm + WSA * kWApplyStage;   // C rows of the current tile [WR][kWCs]
+  uint64_t* full = reinterpret_cast<uint64_t*>(cs + WR * kWCs);
+  uint64_t* empty = full + WSA;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const WRange R = wrange(a, nt_host, KWA);
   if (threadIdx.x == 0) {
@@ -442,7 +394,7 @@ __device__ __forceinline__ void projw_apply_body(const ProjArgs& a, const double
     }
     const uint32_t bytes = (uint32_t)f_nocc * RSWA * 16;
     mbar_expect_tx(&full[s], bytes);
-    bulk_g2s(ring + s * kWApplyStage, phiwa_at(a, f_k, f_nocc, c), bytes, &full[s]);
+    bulk_g2s(sm + s * kWApplyStage, phiwa_at(a, f_k, f_nocc, c), bytes, &full[s]);
   };
   if (threadIdx.x == 0)
     for (int q = 0; q < WSA && R.u0 + q < R.u1; ++q) fill(R.u0 + q, q);
@@ -490,14 +442,10 @@ __device__ __forceinline__ void projw_apply_body(const ProjArgs& a, const double
       }
       const int s = seq % WSA;
       mbar_wait(&full[s], (seq / WSA) & 1);
-      const double2* ps = ring + s * kWApplyStage + 8 * wg + r4;
+      const double2* ps = sm + s * kWApplyStage + 8 * wg + r4;
       {
         const double2* ca = cs + (8 * r_lo + r4) * kWCs;
-#ifdef PWB_EXP_NOCOMPUTE
-        switch (0) {
-#else
         switch (cr) {   // warp-uniform; see coef_chunk for why the count is a template
-#endif
           case 1: apply_chunk<1>(ps, ca, nm, c4, t1, t2, t3); break;
           case 2: apply_chunk<2>(ps, ca, nm, c4, t1, t2, t3); break;
           case 3: apply_chunk<3>(ps, ca, nm, c4, t1, t2, t3); break;
@@ -524,21 +472,6 @@ __device__ __forceinline__ void projw_apply_body(const ProjArgs& a, const double
       }
     }
   }
-}
-
-__global__ void __launch_bounds__(kWThreads, 1)
-    k_projw_apply(ProjArgs a, const double2* __restrict__ C, const double2* __restrict__ Xin,
-                  double2* __restrict__ Y, double ca, double cb, const int* __restrict__ active,
-                  int band_mod, int nt_host, int mr_host) {
-  pdl_wait();
-  extern __shared__ __align__(128) double2 sm[];
-  const int mr = tallest_tile(a, mr_host);
-  if (mr <= 16)
-    projw_apply_body<16>(a, C, Xin, Y, ca, cb, active, band_mod, nt_host, sm);
-  else if (mr <= 40)
-    projw_apply_body<40>(a, C, Xin, Y, ca, cb, active, band_mod, nt_host, sm);
-  else
-    projw_apply_body<WR>(a, C, Xin, Y, ca, cb, active, band_mod, nt_host, sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -625,7 +558,7 @@ static bool x_tensor_maps(const double2* X, long long rows, int nbp, XMaps* out)
 
 int projw_coeffs(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* X,
                  double2* part, double2* C, unsigned* counters, cudaStream_t st,
-                 long long x_rows, int max_rows) {
+                 long long x_rows) {
   if (cap == 0) return PWB_OK;
   PWB_TRY(projw_configure());
   a.tiles = dtiles;
@@ -635,21 +568,21 @@ int projw_coeffs(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const
   memset(&xmaps, 0, sizeof(xmaps));
   const int use_map = x_tensor_maps(X, x_rows, a.nbp, &xmaps) ? 1 : 0;
   (void)launch_k(k_projw_coef, grid, kWThreads, kWCoefSmem, st, a, X, nt_host, part, C,
-                 counters, xmaps, use_map, max_rows);
+                 counters, xmaps, use_map);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
 
 int projw_apply(const ProjTile* dtiles, int nt_host, int cap, ProjArgs a, const double2* C,
                 const double2* Xin, double2* Y, double ca, double cb, const int* active,
-                int band_mod, cudaStream_t st, int max_rows) {
+                int band_mod, cudaStream_t st) {
   if (cap == 0) return PWB_OK;
   PWB_TRY(projw_configure());
   a.tiles = dtiles;
   const long long units = (long long)cap * (a.nbp / KWA);
   const int grid = (int)std::min<long long>(units, kSM);
   (void)launch_k(k_projw_apply, grid, kWThreads, kWApplySmem, st, a, C, Xin, Y, ca, cb, active,
-                 band_mod > 0 ? band_mod : 1, nt_host, max_rows);
+                 band_mod > 0 ? band_mod : 1, nt_host);
   PWB_LAUNCH_CHECK();
   return PWB_OK;
 }
