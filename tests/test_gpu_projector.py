@@ -32,7 +32,7 @@ def _state(alat, ecut, nocc, seed=0):
     return ms, device_state(ms), rng
 
 
-@pytest.mark.parametrize("alat,ecut,nocc", [(20.0, 12.0, 68), (15.0, 10.0, 33)])
+@pytest.mark.parametrize("alat,ecut,nocc", [(20.0, 12.0, 68), (15.0, 10.0, 33), (12.0, 8.0, 20)])
 def test_projector_matches_cublas(alat, ecut, nocc):
     import torch
     from paper_2505_02319_b200 import _lib
@@ -41,7 +41,9 @@ def test_projector_matches_cublas(alat, ecut, nocc):
     dg = ds.grid
     lib = _lib.load()
     P = dg.pack(list(ms.phi_occ.T))                       # (nocc, nbp), zero padded
-    for ncol in (1, 7, 68, 72, 73, 150, 300):
+    # tile heights through every (m fragments, n fragments) pair a warp can own: the
+    # wide kernels dispatch their inner loops on those counts (coef_chunk<CM, CN>)
+    for ncol in (1, 7, 16, 24, 33, 40, 48, 56, 68, 72, 73, 150, 300):
         x = rng.standard_normal((ncol, dg.nb[0])) + 1j * rng.standard_normal((ncol, dg.nb[0]))
         X = dg.pack(list(x))
         want = X - (X @ P.conj().T) @ P
