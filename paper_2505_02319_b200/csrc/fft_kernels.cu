@@ -54,17 +54,33 @@ __global__ void __launch_bounds__(PT, PT == NT ? PWB_FFT_MINB : 1) k_plane_inv(G
   const int nz = FZ::N ? FZ::N : g.nz;
   const int nyz = ny * nz;
   const int nyp = FY::N ? (FY::N % 2 == 0 ? FY::N + 1 : FY::N) : g.nyp;   // odd smem stride
-  for (int i = threadIdx.x; i < nz * nyp; i += PT) sm[i] = make_double2(0.0, 0.0);
-  __syncthreads();
   const int s0 = g.xr[k * (g.nxa + 1) + p];
   const int s1 = g.xr[k * (g.nxa + 1) + p + 1];
   const double2* src = psi + (size_t)row * g.nbp;
   const int* pp = g.ppp + (size_t)k * g.nbp;
-  if (psi2) {
-    const double2* src2 = psi2 + (size_t)row * g.nbp;
-    for (int s = s0 + threadIdx.x; s < s1; s += PT) sm[pp[s]] = cscale(cadd(src[s], src2[s]), scale);
-  } else {
-    for (int s = s0 + threadIdx.x; s < s1; s += PT) sm[pp[s]] = cscale(src[s], scale);
+  // The plane's sphere coefficients (a few per thread) are loaded BEFORE the smem plane
+  // is zeroed and in one batch: the CTA used to zero, synchronise, and then pay one
+  // global-load latency per loop trip (index + value) before its first FFT; without
+  // the butterflies the H apply still took 83% of its time.
+  constexpr int GB = 4;   // loads in flight per thread; more points loop
+  int gi[GB];
+  double2 gv[GB];
+#pragma unroll
+  for (int u = 0; u < GB; ++u) {
+    const int s = s0 + threadIdx.x + u * PT;
+    if (s < s1) {
+      gi[u] = pp[s];
+      gv[u] = psi2 ? cadd(src[s], psi2[(size_t)row * g.nbp + s]) : src[s];
+    }
+  }
+  for (int i = threadIdx.x; i < nz * nyp; i += PT) sm[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < GB; ++u)
+    if (s0 + threadIdx.x + u * PT < s1) sm[gi[u]] = cscale(gv[u], scale);
+  for (int s = s0 + threadIdx.x + GB * PT; s < s1; s += PT) {
+    const double2 v = psi2 ? cadd(src[s], psi2[(size_t)row * g.nbp + s]) : src[s];
+    sm[pp[s]] = cscale(v, scale);
   }
   __syncthreads();
   FZ::template run<PT>(g, sm, g.nya, nyp, 0, g.ya, true);    // z lines of active y
@@ -112,11 +128,30 @@ __global__ void __launch_bounds__(PT, PT == NT ? PWB_FFT_MINB : 1) k_plane_fwd(G
   const double sh = shift ? shift[b] : 0.0;
   if (psi_in) {
     const double2* pin = psi_in + (size_t)b * g.nbp;
-    for (int s = s0 + threadIdx.x; s < s1; s += PT) {
-      const double2 v = sm[pp[s]];
-      const double2 q = pin[s];
-      const double d = kin[s] - sh;
-      dst[s] = make_double2(a * v.x + d * q.x, a * v.y + d * q.y);
+    // all of a thread's index / psi / kinetic loads first, then the smem reads and stores
+    // (one global-load latency at the end of the CTA instead of one per loop trip)
+    constexpr int GB = 4;
+    for (int sb = s0 + threadIdx.x; sb < s1; sb += GB * PT) {
+      int gi[GB];
+      double2 q[GB];
+      double d[GB];
+#pragma unroll
+      for (int u = 0; u < GB; ++u) {
+        const int s = sb + u * PT;
+        if (s < s1) {
+          gi[u] = pp[s];
+          q[u] = pin[s];
+          d[u] = kin[s] - sh;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < GB; ++u) {
+        const int s = sb + u * PT;
+        if (s < s1) {
+          const double2 v = sm[gi[u]];
+          dst[s] = make_double2(a * v.x + d[u] * q[u].x, a * v.y + d[u] * q[u].y);
+        }
+      }
     }
   } else {
     for (int s = s0 + threadIdx.x; s < s1; s += PT) dst[s] = cscale(sm[pp[s]], a);
