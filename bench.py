@@ -257,7 +257,16 @@ def dominant_roofline(ham, proj):
     return dict(proj) if sh.get("projector", 0) >= sh.get("ham_apply", 0) else dict(ham)
 
 
-def oracle_sample(og, dv0, params, budget_s, threads=1):
+def oracle_tolerances(og, dv0, params):
+    """Iteration-0 Sternheimer tolerances of the solve (setup for oracle_sample: ~25 s
+    of host time at configs[4], so the reference arm computes it once, not per step)."""
+    from oracle import dyson as od
+    from oracle import outer as oo
+    spec = oo.parse(params["strategy"], params["tau"], params["m"])
+    return od.tolerance_vector(og, spec, 0, kv_norm=float(np.linalg.norm(dv0)), rhs_norm=1.0)
+
+
+def oracle_sample(og, dv0, params, budget_s, threads=1, tols=None):
     """Bounded CPU sample of the workload: the oracle's RHS + Sternheimer solves of
     the first (k, n) pairs at the solve's iteration-0 tolerances, band-applies/s.
 
@@ -272,9 +281,9 @@ def oracle_sample(og, dv0, params, budget_s, threads=1):
     from oracle import model as om
     from oracle import outer as oo
     from oracle import response as orsp
-    spec = oo.parse(params["strategy"], params["tau"], params["m"])
     nrm = float(np.linalg.norm(dv0))
-    tols = od.tolerance_vector(og, spec, 0, kv_norm=nrm, rhs_norm=1.0)
+    if tols is None:
+        tols = oracle_tolerances(og, dv0, params)
     blocks = og.blocks if hasattr(og, "blocks") else [og]
     pairs, off = [], 0
     for blk in blocks:                      # (k, n) pairs in the solve's order
@@ -577,9 +586,10 @@ def run_reference(args):
               "reference": setup}
     if hasattr(og, "blocks") or og.grids.n_g > 100000:
         vals = []
+        tols0 = oracle_tolerances(og, dv0, params)
         t_all = time.perf_counter()
         for _ in range(args.warmup + args.steps):
-            v, sample = oracle_sample(og, dv0, params, 10.0, threads=ncores)
+            v, sample = oracle_sample(og, dv0, params, 10.0, threads=ncores, tols=tols0)
             vals.append(v)
         value = float(np.mean(vals[args.warmup:]))
         line = dict(common, value=value,
